@@ -1,0 +1,192 @@
+/*
+ * bbmm.h -- C-ABI of the B200-native BBMM hot path (arXiv 1809.11165).
+ *
+ * The library computes, for an exact Gaussian process with kernel matrix
+ * Khat = K(X,X) + sigma^2 I, the three inference terms of the paper's Sec. 4
+ * (Khat^{-1} y, log|Khat|, Tr(Khat^{-1} dKhat/dtheta)) with
+ * ONE call of modified batched preconditioned conjugate gradients (mBCG,
+ * Alg. S2) on the block [y, z_1..z_t],
+ * preconditioned by a rank-k pivoted Cholesky factor applied through
+ * Woodbury (App. B), and from them the
+ * marginal log likelihood and its gradient (Eq. 2).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Pointers named *_d are DEVICE pointers on the context's device, owned by
+ *    the caller; pointers named *_h are HOST pointers owned by the caller.
+ *    The library owns only its workspace (inside the context).
+ *  - Matrices are row-major.  X_d is n x d fp32 (every rank holds all n rows).
+ *  - Work is enqueued on the context stream; a call returns after its _h
+ *    outputs are written (it synchronises the stream only to deliver them).
+ *  - Multi-GPU (bbmm_ctx_set_comm with nranks > 1): rank r owns the rows
+ *    [r*nb, min(n, (r+1)*nb)) with nb = ceil(n / nranks) ("local rows").
+ *    All ranks call collectively with identical scalar arguments; returned
+ *    scalars are identical on all ranks.  Per iteration the library
+ *    all-gathers the search directions and all-reduces per-column dot
+ *    products over NCCL.
+ *  - Hyperparameters theta = (log l_1..log l_{n_ls}, log s, log sigma):
+ *    l = lengthscale(s) (n_ls = 1 isotropic, n_ls = d ARD), s = outputscale,
+ *    sigma^2 = exp(2 log sigma) = noise variance (reading R3).
+ *  - Kernels (readings R1/R2), r^2 = sum_q (x_q - x'_q)^2/l_q^2:
+ *      BBMM_RBF:      k = s exp(-r^2 / 2)
+ *      BBMM_MATERN52: k = s (1 + sqrt(5) r + 5 r^2 / 3) exp(-sqrt(5) r)
+ *  - Errors: every function returns a bbmm_status_t; arguments are validated
+ *    before anything is launched (BBMM_ERR_ARG); no exception crosses the
+ *    ABI; bbmm_last_error() returns a text description of the last failure
+ *    on that context.  Non-convergence within max_iter is NOT an error
+ *    (iteration counts / residuals report it); pivoted Cholesky running out
+ *    of positive pivots is NOT an error (k_used < k).
+ */
+#ifndef BBMM_H_
+#define BBMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bbmm_ctx_s *bbmm_ctx_t;
+
+typedef enum {
+    BBMM_OK = 0,
+    BBMM_ERR_ARG = 2,      /* invalid argument (shape, range, null pointer) */
+    BBMM_ERR_DATA = 3,     /* non-finite input data */
+    BBMM_ERR_NUMERIC = 4,  /* breakdown: alpha <= 0 / non-finite (indefinite
+                              operator), Ritz value <= 0, chol(C) failed */
+    BBMM_ERR_CUDA = 5,
+    BBMM_ERR_NCCL = 6,
+    BBMM_ERR_OOM = 7
+} bbmm_status_t;
+
+typedef enum { BBMM_RBF = 0, BBMM_MATERN52 = 1 } bbmm_kernel_t;
+
+/* How the blackbox matmul Khat*M is performed:
+ * ON-THE-FLY never materialises K (every kernel entry recomputed per matmul);
+ * STORED materialises this rank's K row block (local rows x n fp32) once per
+ * call and streams it from HBM every iteration. */
+typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
+
+typedef struct {
+    int32_t kind;            /* bbmm_kernel_t */
+    int32_t n_ls;            /* 1 (isotropic) or d (ARD) */
+    const double *log_ls_h;  /* host, n_ls entries */
+    double log_outputscale;  /* log s */
+    double log_noise;        /* log sigma */
+} bbmm_hyper_t;
+
+/* Diagnostics of one bbmm_mll_and_grad call (host struct). */
+typedef struct {
+    int32_t iters;           /* K-hat matmuls performed by mBCG */
+    int32_t k_used;          /* pivoted-Cholesky rank actually used */
+    double logdet_precond;   /* log|Phat| (determinant lemma) */
+    double logdet_ratio;     /* SLQ estimate of log|Phat^{-1} Khat| */
+    double logdet;           /* log|Khat| = sum of the two */
+    double quad_y;           /* y^T Khat^{-1} y (y^T u_0) */
+    double resid_trace;      /* tr(K - L L^T) after pivoted Cholesky */
+    double relres_y;         /* ||r_y|| / ||y|| at exit */
+    double ms_total;         /* device time of the whole call (CUDA events) */
+    double ms_pivchol;       /* pivoted Cholesky + preconditioner setup */
+    double ms_mbcg;          /* probes + mBCG loop (incl. collectives) */
+    double ms_matmul;        /* sum over mBCG iterations of the K-hat*D kernel */
+    double ms_slq;           /* tridiagonal eigensolves + SLQ */
+    double ms_deriv;         /* derivative pass */
+    int32_t matmul_launches; /* K-hat*D kernel launches inside ms_matmul */
+    int32_t gpu_launches;    /* library kernels launched by the call */
+} bbmm_stats_t;
+
+/* ---- context ----------------------------------------------------------- */
+
+/* Create a context bound to CUDA `device`, enqueueing on `cuda_stream`
+ * (a cudaStream_t; NULL = a stream the context creates and owns). */
+bbmm_status_t bbmm_ctx_create(int device, void *cuda_stream, bbmm_ctx_t *out);
+bbmm_status_t bbmm_ctx_destroy(bbmm_ctx_t ctx);
+/* Text of the last error on `ctx` (static storage owned by ctx). */
+const char *bbmm_last_error(bbmm_ctx_t ctx);
+/* Library version string. */
+const char *bbmm_version(void);
+
+/* Multi-GPU: rank 0 calls bbmm_nccl_unique_id, broadcasts the 128 bytes to
+ * all ranks (e.g. torch.distributed.broadcast), then every rank calls
+ * bbmm_ctx_set_comm (collective; creates an NCCL communicator). */
+bbmm_status_t bbmm_nccl_unique_id(void *out_128_bytes);
+bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank,
+                                const void *nccl_unique_id_128_bytes);
+/* Local row range [*r0, *r1) of this rank for problem size n. */
+bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0,
+                              int64_t *r1);
+
+/* ---- entry points ------------------------------------------------------ */
+
+/* Blackbox matmul V = Khat * D (the K1/K2 kernel
+ * alone -- the "kernel-matmul" of the metric).
+ *   D_d: n x ncols fp64, leading dim ldd (all n rows, every rank).
+ *   V_d: (local rows) x ncols fp64, leading dim ldv.
+ *   1 <= ncols <= 64, 1 <= d <= 32. */
+bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X_d, int64_t n,
+                                 int32_t d, const bbmm_hyper_t *hyper,
+                                 bbmm_kmode_t kmode, const double *D_d,
+                                 int32_t ncols, int64_t ldd, double *V_d,
+                                 int64_t ldv);
+
+/* Rank-k pivoted Cholesky of K_XX (no noise term; App. B PAPER.md:80-135,
+ * PAPER.md:729-735), fp64, pivots = argmax of the remaining Schur diagonal
+ * with ties broken by the lowest index; stops early when the maximum is
+ * <= 1e-12 * s (then k_used < k).  Replicated: every rank computes all n.
+ *   L_d: k x n fp64 (row m = column m of the n x k factor, contiguous over
+ *        the n points; rows >= k_used are zero).
+ *   pivots_h: k int64 (entries >= k_used are -1). */
+bbmm_status_t bbmm_pivchol(bbmm_ctx_t ctx, const float *X_d, int64_t n,
+                           int32_t d, const bbmm_hyper_t *hyper, int32_t k,
+                           double *L_d, int64_t *pivots_h, int32_t *k_used_h,
+                           double *resid_trace_h);
+
+/* mBCG (Alg. S2, textbook signs, R5-R9) on
+ * Khat with preconditioner Phat = L L^T + sigma^2 I applied via Woodbury
+ * (k >= 1) or no preconditioner (k == 0, L_d ignored).
+ *   L_d: k x n fp64 as returned by bbmm_pivchol (full n on every rank).
+ *   B_d, U_d: (local rows) x ncols fp64, leading dims ldb / ldu.
+ *   Columns [ncols - n_tridiag, ncols) are probe columns whose Lanczos
+ *   coefficients are returned (all columns' alpha/beta are returned anyway).
+ *   tol: a column is frozen once ||r_c|| / ||b_c|| < tol; tol == 0 runs
+ *   exactly max_iter iterations.  1 <= ncols <= 64.
+ *   alpha_h, beta_h: max_iter x ncols host fp64 (row j = iteration j; 0 where
+ *   not computed);  iters_h: ncols int32 (alphas recorded per column);
+ *   relres_h: ncols fp64;  rho0_h: ncols fp64 (b^T Phat^{-1} b), may be NULL. */
+bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X_d, int64_t n, int32_t d,
+                        const bbmm_hyper_t *hyper, bbmm_kmode_t kmode,
+                        const double *L_d, int32_t k, const double *B_d,
+                        int32_t ncols, int64_t ldb, int32_t max_iter,
+                        double tol, double *U_d, int64_t ldu, double *alpha_h,
+                        double *beta_h, int32_t *iters_h, double *relres_h,
+                        double *rho0_h);
+
+/* One-call exact-GP marginal log likelihood and gradient (north-star entry):
+ *   pivchol(k) -> Phat -> probes z_i = L eps1_i + sigma eps2_i (k >= 1; plain
+ *   Rademacher eps2_i when k == 0) -> one mBCG on [y, z_1..z_t] -> SLQ
+ *   log|Khat| -> one derivative pass -> mll, grad.
+ *   mll = -1/2 (y^T u_0 + log|Khat| + n log 2 pi)
+ *   grad_q = 1/2 (u_0^T dKhat_q u_0 - (1/t) sum_i u_i^T dKhat_q Phat^{-1} z_i)
+ * Inputs: X_d n x d fp32, y_d n fp32 (all rows on every rank).
+ *   eps_d: NULL -> probe signs from the counter-based generator with `seed`
+ *          (DESIGN.md "Probe generator"); else (n + k) x t int8 in {-1, +1}
+ *          device array (rows < n: eps2, rows >= n: eps1).
+ *   1 <= t <= 63, 0 <= k <= min(n, 128), max_iter >= 1, tol >= 0.
+ * Outputs: mll_h (1), grad_h (n_ls + 2: d/dlog l_q..., d/dlog s,
+ *   d/dlog sigma), stats_h (may be NULL).
+ * Optional outputs (NULL to skip): U_d (local rows) x (t+1) fp64 solves
+ *   [Khat^{-1} y, Khat^{-1} z_1..]; pivots_h (k int64). */
+bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X_d,
+                                const float *y_d, int64_t n, int32_t d,
+                                const bbmm_hyper_t *hyper, bbmm_kmode_t kmode,
+                                int32_t t, int32_t k, int32_t max_iter,
+                                double tol, uint64_t seed, const int8_t *eps_d,
+                                double *mll_h, double *grad_h,
+                                bbmm_stats_t *stats_h, double *U_d,
+                                int64_t *pivots_h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBMM_H_ */

@@ -1,0 +1,547 @@
+// bbmm_api.cu -- the C-ABI of include/bbmm.h: argument validation, context
+// and workspace management, NCCL plumbing, and the orchestration of the
+// one-call MLL + gradient ("a single call to mBCG").
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+
+#include "bbmm_internal.cuh"
+
+namespace bbmm {
+
+// ------------------------------------------------------------- workspace
+void *Workspace::get(const std::string &name, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 256);
+    auto it = bufs.find(name);
+    if (it != bufs.end()) {
+        if (it->second.second >= bytes) return it->second.first;
+        BBMM_CUDA(cudaFree(it->second.first));
+        bufs.erase(it);
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{BBMM_ERR_OOM, "cudaMalloc of workspace '" + name + "' (" +
+                                      std::to_string(bytes) + " bytes) failed"};
+    }
+    bufs[name] = {p, bytes};
+    return p;
+}
+
+void Workspace::release_all() {
+    for (auto &kv : bufs) cudaFree(kv.second.first);
+    bufs.clear();
+}
+
+RowRange local_rows(const bbmm_ctx_s *ctx, int64_t n) {
+    RowRange r;
+    r.nb = ceil_div(n, ctx->nranks);
+    r.r0 = std::min<int64_t>(n, (int64_t)ctx->rank * r.nb);
+    r.r1 = std::min<int64_t>(n, r.r0 + r.nb);
+    return r;
+}
+
+Hyper make_hyper(const bbmm_hyper_t *hp, int d) {
+    BBMM_REQUIRE(hp != nullptr, "hyper is NULL");
+    BBMM_REQUIRE(hp->kind == BBMM_RBF || hp->kind == BBMM_MATERN52, "unknown kernel kind");
+    BBMM_REQUIRE(hp->n_ls == 1 || hp->n_ls == d, "n_ls must be 1 or d");
+    BBMM_REQUIRE(hp->log_ls_h != nullptr, "log_ls_h is NULL");
+    Hyper h;
+    h.kind = hp->kind;
+    h.n_ls = hp->n_ls;
+    for (int q = 0; q < hp->n_ls; q++) {
+        BBMM_REQUIRE(std::isfinite(hp->log_ls_h[q]), "non-finite log lengthscale");
+        h.ls[q] = std::exp(hp->log_ls_h[q]);
+    }
+    BBMM_REQUIRE(std::isfinite(hp->log_outputscale) && std::isfinite(hp->log_noise),
+                 "non-finite hyperparameter");
+    h.s = std::exp(hp->log_outputscale);
+    h.noise_var = std::exp(2.0 * hp->log_noise);
+    h.sigma = std::exp(hp->log_noise);
+    return h;
+}
+
+// ------------------------------------------------------------------ comm
+void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count) {
+    if (ctx->nranks <= 1) return;
+    BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank) {
+    if (ctx->nranks <= 1) return;
+    char *b = (char *)buf;
+    BBMM_NCCL(ncclAllGather(b + (size_t)ctx->rank * bytes_per_rank, b, bytes_per_rank, ncclChar,
+                            ctx->comm, ctx->stream));
+}
+
+namespace {
+
+// D (fp64, rows [r0, r0+rows) of an n x c block, ld) -> D32 rows at the same
+// global positions, fp32, stride cs (zero padding columns).
+__global__ void k_pack_d32(const double *__restrict__ D, int64_t ldd, int64_t rows, int c,
+                           int64_t row_off, int cs, float *__restrict__ D32) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cs;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / cs;
+        int col = (int)(e - i * cs);
+        D32[(row_off + i) * cs + col] = col < c ? (float)D[i * ldd + col] : 0.0f;
+    }
+}
+
+// V[i][col] = sum_s Vpart[s][i][col] + sigma^2 D[r0+i][col]
+__global__ void k_matmul_finish(const double *__restrict__ Vpart, int splits, int cs, int64_t nloc,
+                                int c, double noise_var, const double *__restrict__ D,
+                                int64_t ldd, int64_t r0, double *__restrict__ V, int64_t ldv) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * c;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / c;
+        int col = (int)(e - i * c);
+        double v = 0.0;
+        for (int s = 0; s < splits; s++) v += Vpart[((int64_t)s * nloc + i) * cs + col];
+        V[i * ldv + col] = v + noise_var * D[(r0 + i) * ldd + col];
+    }
+}
+
+// Derivative-pass operands: A32 = [U_1..U_t, U_0] (local rows),
+// B32 rows at global positions = [Z0_1..Z0_t / t, -U_0] ; stride cs.
+__global__ void k_pack_deriv(const double *__restrict__ U, const double *__restrict__ Z0,
+                             int64_t nloc, int t, int cs, int64_t r0, float *__restrict__ A32,
+                             float *__restrict__ B32) {
+    const int c = t + 1;
+    const double inv_t = 1.0 / (double)t;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * cs;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / cs;
+        int col = (int)(e - i * cs);
+        float a = 0.0f, b = 0.0f;
+        if (col < t) {
+            a = (float)U[i * c + 1 + col];
+            b = (float)(Z0[i * c + 1 + col] * inv_t);
+        } else if (col == t) {
+            a = (float)U[i * c];
+            b = (float)(-U[i * c]);
+        }
+        A32[i * cs + col] = a;
+        B32[(r0 + i) * cs + col] = b;
+    }
+}
+
+// Local scalar terms: out[0] = y^T u0, out[1] = u0^T u0, out[2] = sum_i u_i^T Z0_i
+__global__ void k_scalar_terms(const double *__restrict__ U, const double *__restrict__ Z0,
+                               const float *__restrict__ y, int64_t r0, int64_t nloc, int t,
+                               double *__restrict__ part) {
+    const int c = t + 1;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double u0 = U[i * c];
+        a0 += (double)y[r0 + i] * u0;
+        a1 += u0 * u0;
+        for (int q = 1; q <= t; q++) a2 += U[i * c + q] * Z0[i * c + q];
+    }
+    __shared__ double sh[3][256];
+    sh[0][threadIdx.x] = a0;
+    sh[1][threadIdx.x] = a1;
+    sh[2][threadIdx.x] = a2;
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int u = 0; u < 256; u++) s += sh[threadIdx.x][u];
+        part[blockIdx.x * 3 + threadIdx.x] = s;
+    }
+}
+
+__global__ void k_check_finite(const float *__restrict__ x, int64_t n, int *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) atomicExch(bad, 1);
+}
+
+int grid_for(int64_t work) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 8 * kNumSMs));
+}
+
+void check_finite(bbmm_ctx_s *ctx, const float *x, int64_t n, const char *what) {
+    int *bad = (int *)ctx->ws.get("finite_flag", sizeof(int));
+    BBMM_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    k_check_finite<<<grid_for(n), 256, 0, ctx->stream>>>(x, n, bad);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+    int h = 0;
+    BBMM_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) throw Error{BBMM_ERR_DATA, std::string("non-finite values in ") + what};
+}
+
+struct Timer {
+    cudaEvent_t e;
+    explicit Timer(cudaStream_t s) {
+        BBMM_CUDA(cudaEventCreate(&e));
+        BBMM_CUDA(cudaEventRecord(e, s));
+    }
+    ~Timer() { cudaEventDestroy(e); }
+    float since(const Timer &o) const {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, o.e, e);
+        return ms;
+    }
+};
+
+void validate_common(bbmm_ctx_s *ctx, const float *X, int64_t n, int d) {
+    BBMM_REQUIRE(ctx != nullptr, "ctx is NULL");
+    BBMM_REQUIRE(X != nullptr, "X is NULL");
+    BBMM_REQUIRE(n >= 1, "n must be >= 1");
+    BBMM_REQUIRE(d >= 1 && d <= kMaxDim, "d must be in [1, 32]");
+}
+
+template <typename F>
+bbmm_status_t guarded(bbmm_ctx_s *ctx, F &&f) {
+    try {
+        if (ctx) BBMM_CUDA(cudaSetDevice(ctx->device));
+        f();
+        return BBMM_OK;
+    } catch (const Error &e) {
+        if (ctx) ctx->err = e.msg;
+        return e.st;
+    } catch (const std::exception &e) {
+        if (ctx) ctx->err = e.what();
+        return BBMM_ERR_CUDA;
+    }
+}
+
+}  // namespace
+}  // namespace bbmm
+
+using namespace bbmm;
+
+extern "C" {
+
+const char *bbmm_version(void) { return "bbmm-b200 0.1 (sm_100a)"; }
+
+bbmm_status_t bbmm_ctx_create(int device, void *cuda_stream, bbmm_ctx_t *out) {
+    if (!out) return BBMM_ERR_ARG;
+    *out = nullptr;
+    bbmm_ctx_s *ctx = new bbmm_ctx_s();
+    ctx->device = device;
+    bbmm_status_t st = guarded(ctx, [&] {
+        if (cuda_stream) {
+            ctx->stream = (cudaStream_t)cuda_stream;
+        } else {
+            BBMM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+    });
+    if (st != BBMM_OK) {
+        delete ctx;
+        return st;
+    }
+    *out = ctx;
+    return BBMM_OK;
+}
+
+bbmm_status_t bbmm_ctx_destroy(bbmm_ctx_t ctx) {
+    if (!ctx) return BBMM_ERR_ARG;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ctx->ws.release_all();
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return BBMM_OK;
+}
+
+const char *bbmm_last_error(bbmm_ctx_t ctx) { return ctx ? ctx->err.c_str() : "ctx is NULL"; }
+
+bbmm_status_t bbmm_nccl_unique_id(void *out) {
+    if (!out) return BBMM_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return BBMM_ERR_NCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return BBMM_OK;
+}
+
+bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void *uid) {
+    return guarded(ctx, [&] {
+        BBMM_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+        if (ctx->comm) {
+            ncclCommDestroy(ctx->comm);
+            ctx->comm = nullptr;
+        }
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+        if (nranks > 1) {
+            BBMM_REQUIRE(uid != nullptr, "unique id is NULL");
+            ncclUniqueId id;
+            std::memcpy(&id, uid, sizeof(id));
+            BBMM_NCCL(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+        }
+    });
+}
+
+bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0, int64_t *r1) {
+    if (!ctx || !r0 || !r1 || n < 0) return BBMM_ERR_ARG;
+    RowRange rr = local_rows(ctx, n);
+    *r0 = rr.r0;
+    *r1 = rr.r1;
+    return BBMM_OK;
+}
+
+bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
+                                 const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, const double *D,
+                                 int32_t ncols, int64_t ldd, double *V, int64_t ldv) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(D && V, "D / V is NULL");
+        BBMM_REQUIRE(ncols >= 1 && ncols <= kMaxCols, "ncols must be in [1, 64]");
+        BBMM_REQUIRE(ldd >= ncols && ldv >= ncols, "leading dimension < ncols");
+        BBMM_REQUIRE(kmode == BBMM_ONTHEFLY || kmode == BBMM_STORED, "bad kmode");
+        RowRange rr = local_rows(ctx, n);
+        const int64_t nloc = rr.count();
+        const int dp = pad_dim(d), cp = pad_cols(ncols), cs = (cp + 3) & ~3, ds = (dp + 3) & ~3;
+        float *Xs = (float *)ctx->ws.get("Xs", (size_t)n * ds * 4);
+        scale_inputs(ctx, X, n, d, h, Xs, dp);
+        float *D32 = (float *)ctx->ws.get("mm_D32", (size_t)n * cs * 4);
+        k_pack_d32<<<grid_for(n * cs), 256, 0, ctx->stream>>>(D, ldd, n, ncols, 0, cs, D32);
+        BBMM_LAUNCH_CHECK();
+        ctx->launches++;
+        if (nloc == 0) return;
+        const bool stored = kmode == BBMM_STORED;
+        size_t cap = vpart_elems(n, nloc, cp, stored);
+        double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
+        int splits;
+        if (stored) {
+            const int64_t ldk = ((n + 3) / 4) * 4;
+            float *Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
+            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
+            splits = kernel_matmul_stored(ctx, Kst, n, nloc, D32, cp, Vpart, cap, nullptr, nullptr);
+        } else {
+            splits = kernel_matmul_onthefly(ctx, h.kind, Xs, dp, n, rr.r0, nloc, D32, cp, h.s, Vpart,
+                                            cap, nullptr, nullptr);
+        }
+        k_matmul_finish<<<grid_for(nloc * ncols), 256, 0, ctx->stream>>>(
+            Vpart, splits, cs, nloc, ncols, h.noise_var, D, ldd, rr.r0, V, ldv);
+        BBMM_LAUNCH_CHECK();
+        ctx->launches++;
+        BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+bbmm_status_t bbmm_pivchol(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
+                           const bbmm_hyper_t *hyper, int32_t k, double *L, int64_t *piv_h,
+                           int32_t *k_used_h, double *resid_h) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
+        BBMM_REQUIRE(k == 0 || L != nullptr, "L is NULL");
+        int ku = 0;
+        double res = 0.0;
+        std::vector<int64_t> piv(std::max(k, 1));
+        pivchol(ctx, X, n, d, h, k, L, piv.data(), &ku, &res);
+        if (piv_h) std::copy(piv.begin(), piv.begin() + k, piv_h);
+        if (k_used_h) *k_used_h = ku;
+        if (resid_h) *resid_h = res;
+    });
+}
+
+bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
+                        const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, const double *L, int32_t k,
+                        const double *B, int32_t ncols, int64_t ldb, int32_t max_iter, double tol,
+                        double *U, int64_t ldu, double *alpha_h, double *beta_h, int32_t *iters_h,
+                        double *relres_h, double *rho0_h) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
+        BBMM_REQUIRE(k == 0 || L != nullptr, "L is NULL");
+        BBMM_REQUIRE(B && U, "B / U is NULL");
+        BBMM_REQUIRE(ncols >= 1 && ncols <= kMaxCols, "ncols must be in [1, 64]");
+        BBMM_REQUIRE(ldb >= ncols && ldu >= ncols, "leading dimension < ncols");
+        BBMM_REQUIRE(max_iter >= 1 && max_iter <= 256, "max_iter must be in [1, 256]");
+        BBMM_REQUIRE(tol >= 0.0 && std::isfinite(tol), "tol must be >= 0");
+        RowRange rr = local_rows(ctx, n);
+        const int64_t nloc = rr.count();
+        const int dp = pad_dim(d), cp = pad_cols(ncols), ds = (dp + 3) & ~3;
+        float *Xs = (float *)ctx->ws.get("Xs", (size_t)n * ds * 4);
+        scale_inputs(ctx, X, n, d, h, Xs, dp);
+        double *cholC = (double *)ctx->ws.get("cholC", (size_t)std::max(k, 1) * std::max(k, 1) * 8);
+        double *ldp = (double *)ctx->ws.get("logdet_pre", 8);
+        precond_setup(ctx, L, n, k, h.noise_var, cholC, ldp);
+        float *Kst = nullptr;
+        if (kmode == BBMM_STORED && nloc > 0) {
+            const int64_t ldk = ((n + 3) / 4) * 4;
+            Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
+            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
+        }
+        MbcgArgs a{Xs, dp, h.kind, h.s, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L, k, ncols,
+                   max_iter, tol};
+        MbcgOut o;
+        o.U = U;
+        o.ldu = ldu;
+        mbcg_run(ctx, a, B, ldb, cholC, o);
+        if (alpha_h) std::copy(o.alpha.begin(), o.alpha.end(), alpha_h);
+        if (beta_h) std::copy(o.beta.begin(), o.beta.end(), beta_h);
+        if (iters_h) std::copy(o.iters.begin(), o.iters.end(), iters_h);
+        if (relres_h) std::copy(o.relres.begin(), o.relres.end(), relres_h);
+        if (rho0_h) std::copy(o.rho0.begin(), o.rho0.end(), rho0_h);
+    });
+}
+
+bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, int64_t n,
+                                int32_t d, const bbmm_hyper_t *hyper, bbmm_kmode_t kmode,
+                                int32_t t, int32_t k, int32_t max_iter, double tol, uint64_t seed,
+                                const int8_t *eps, double *mll_h, double *grad_h,
+                                bbmm_stats_t *stats_h, double *U_out, int64_t *pivots_h) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(y != nullptr, "y is NULL");
+        BBMM_REQUIRE(t >= 1 && t + 1 <= kMaxCols, "t must be in [1, 63]");
+        BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
+        BBMM_REQUIRE(max_iter >= 1 && max_iter <= 256, "max_iter must be in [1, 256]");
+        BBMM_REQUIRE(tol >= 0.0 && std::isfinite(tol), "tol must be >= 0");
+        BBMM_REQUIRE(mll_h && grad_h, "mll_h / grad_h is NULL");
+        BBMM_REQUIRE(kmode == BBMM_ONTHEFLY || kmode == BBMM_STORED, "bad kmode");
+        cudaStream_t sm = ctx->stream;
+        const int launches0 = ctx->launches;
+        check_finite(ctx, X, n * d, "X");
+        check_finite(ctx, y, n, "y");
+        Timer t_start(sm);
+        const int c = t + 1;
+        RowRange rr = local_rows(ctx, n);
+        const int64_t nloc = rr.count();
+        const int dp = pad_dim(d), cp = pad_cols(c), cs = (cp + 3) & ~3, ds = (dp + 3) & ~3;
+        Workspace &ws = ctx->ws;
+        float *Xs = (float *)ws.get("Xs", (size_t)n * ds * 4);
+        scale_inputs(ctx, X, n, d, h, Xs, dp);
+
+        // 1. pivoted Cholesky + preconditioner (Sec. 4.1, App. B)
+        double *L = (double *)ws.get("L", (size_t)std::max(k, 1) * n * 8);
+        int k_used = 0;
+        double resid = 0.0;
+        std::vector<int64_t> piv(std::max(k, 1), -1);
+        if (k > 0) pivchol(ctx, X, n, d, h, k, L, piv.data(), &k_used, &resid);
+        else resid = h.s * (double)n;
+        double *cholC = (double *)ws.get("cholC", (size_t)std::max(k, 1) * std::max(k, 1) * 8);
+        double *scal = (double *)ws.get("scalars", 16 * 8);   // [logdet_pre, logdet_ratio, ...]
+        int *status = (int *)ws.get("status", sizeof(int));
+        BBMM_CUDA(cudaMemsetAsync(status, 0, sizeof(int), sm));
+        precond_setup(ctx, L, n, k > 0 ? k_used : 0, h.noise_var, cholC, scal + 0);
+        Timer t_pc(sm);
+
+        // 2. probes and B = [y | Z] (Eq. 3)
+        double *B = (double *)ws.get("B", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
+        double *Z0 = (double *)ws.get("Z0", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
+        if (nloc > 0)
+            make_probes(ctx, eps, seed, n, k, t, L, k > 0 ? k_used : 0, k > 0 ? h.sigma : 1.0,
+                        rr.r0, nloc, y, B, c);
+        float *Kst = nullptr;
+        if (kmode == BBMM_STORED && nloc > 0) {
+            const int64_t ldk = ((n + 3) / 4) * 4;
+            Kst = (float *)ws.get("Kst", (size_t)nloc * ldk * 4);
+            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
+        }
+
+        // 3. one mBCG call on [y, z_1..z_t]
+        MbcgArgs a{Xs, dp, h.kind, h.s, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
+                   k > 0 ? k_used : 0, c, max_iter, tol};
+        MbcgOut o;
+        o.Z0 = Z0;
+        mbcg_run(ctx, a, B, c, cholC, o);
+        Timer t_cg(sm);
+
+        // 4. SLQ log-det (probe columns 1..t)
+        const char *stb = reinterpret_cast<const char *>(o.state_d);
+        slq_logdet(ctx, o.ahist_d, o.bhist_d,
+                   reinterpret_cast<const int *>(stb + offsetof(MbcgState, iters)),
+                   reinterpret_cast<const double *>(stb + offsetof(MbcgState, rho0)), max_iter, c,
+                   1, t, scal + 1, status);
+        Timer t_slq(sm);
+
+        // 5. derivative pass (once)
+        float *A32 = (float *)ws.get("A32", (size_t)std::max<int64_t>(nloc, 1) * cs * 4);
+        float *B32 = (float *)ws.get("B32", (size_t)rr.nb * ctx->nranks * cs * 4);
+        BBMM_CUDA(cudaMemsetAsync(B32, 0, (size_t)rr.nb * ctx->nranks * cs * 4, sm));
+        if (nloc > 0) {
+            k_pack_deriv<<<grid_for(nloc * cs), 256, 0, sm>>>(o.U_d, Z0, nloc, t, cs, rr.r0, A32,
+                                                             B32);
+            ctx->launches++;
+        }
+        allgather_rows(ctx, B32, (size_t)rr.nb * cs * 4);
+        const int nq = dp + 1;
+        double *dpart = (double *)ws.get("d_part", derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp) * 8);
+        double *dred = (double *)ws.get("d_red", (size_t)(nq + 3) * 8);
+        BBMM_CUDA(cudaMemsetAsync(dred, 0, (size_t)(nq + 3) * 8, sm));
+        const int sblk = grid_for(std::max<int64_t>(nloc, 1));
+        double *spart = (double *)ws.get("s_part", (size_t)sblk * 3 * 8);
+        if (nloc > 0) {
+            int nblk = 0;
+            derivative_pass(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, nq, h.n_ls > 1, d,
+                            dpart, &nblk);
+            reduce_blocks(ctx, dpart, nblk, nq, dred);
+            k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
+            ctx->launches++;
+            reduce_blocks(ctx, spart, sblk, 3, dred + nq);
+        }
+        allreduce_sum(ctx, dred, (size_t)nq + 3);
+        BBMM_LAUNCH_CHECK();
+        Timer t_end(sm);
+
+        // 6. assemble (fp64, host): Eq. 2 with reading R4
+        std::vector<double> hred(nq + 3);
+        double hs[2];
+        int st_h = 0;
+        BBMM_CUDA(cudaMemcpyAsync(hred.data(), dred, (size_t)(nq + 3) * 8, cudaMemcpyDeviceToHost, sm));
+        BBMM_CUDA(cudaMemcpyAsync(hs, scal, 2 * 8, cudaMemcpyDeviceToHost, sm));
+        BBMM_CUDA(cudaMemcpyAsync(&st_h, status, sizeof(int), cudaMemcpyDeviceToHost, sm));
+        BBMM_CUDA(cudaStreamSynchronize(sm));
+        if (st_h) throw Error{BBMM_ERR_NUMERIC, "non-positive Ritz value in SLQ (Khat not PD?)"};
+        const double logdet = hs[0] + hs[1];
+        const double quad_y = hred[nq + 0], uu = hred[nq + 1], uz = hred[nq + 2];
+        *mll_h = -0.5 * (quad_y + logdet + (double)n * std::log(2.0 * M_PI));
+        // lengthscale / outputscale components: grad = -S/2 with constants
+        const double lfac = (h.kind == BBMM_RBF) ? h.s * 2.0 * std::log(2.0) : h.s / 3.0;
+        if (h.n_ls == 1) {
+            double sl = 0.0;
+            for (int q = 0; q < d; q++) sl += hred[q];
+            grad_h[0] = -0.5 * lfac * sl;
+        } else {
+            for (int q = 0; q < d; q++) grad_h[q] = -0.5 * lfac * hred[q];
+        }
+        grad_h[h.n_ls] = -0.5 * h.s * hred[dp];
+        // log sigma: dKhat = 2 sigma^2 I
+        const double tau_s = 2.0 * h.noise_var * uz / (double)t;
+        const double quad_s = 2.0 * h.noise_var * uu;
+        grad_h[h.n_ls + 1] = 0.5 * (quad_s - tau_s);
+
+        if (U_out && nloc > 0)
+            BBMM_CUDA(cudaMemcpyAsync(U_out, o.U_d, (size_t)nloc * c * 8, cudaMemcpyDeviceToDevice, sm));
+        if (pivots_h) std::copy(piv.begin(), piv.begin() + k, pivots_h);
+        if (stats_h) {
+            bbmm_stats_t s{};
+            s.iters = o.iters_run;
+            s.k_used = k_used;
+            s.logdet_precond = hs[0];
+            s.logdet_ratio = hs[1];
+            s.logdet = logdet;
+            s.quad_y = quad_y;
+            s.resid_trace = resid;
+            s.relres_y = o.relres.empty() ? 0.0 : o.relres[0];
+            s.ms_total = t_end.since(t_start);
+            s.ms_pivchol = t_pc.since(t_start);
+            s.ms_mbcg = t_cg.since(t_pc);
+            s.ms_matmul = o.ms_matmul;
+            s.ms_slq = t_slq.since(t_cg);
+            s.ms_deriv = t_end.since(t_slq);
+            s.matmul_launches = o.matmul_launches;
+            s.gpu_launches = ctx->launches - launches0;
+            *stats_h = s;
+        }
+        BBMM_CUDA(cudaStreamSynchronize(sm));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+// bbmm_internal.cuh -- shared declarations of the CUDA path (sm_100a).
+// Nothing here is shared with oracle/ (independent implementations).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/bbmm.h"
+
+namespace bbmm {
+
+constexpr int kMaxCols = 64;     // ncols = t + 1 <= 64
+constexpr int kMaxRank = 128;    // preconditioner rank k
+constexpr int kMaxDim = 32;      // input dimension d
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------- status
+struct Error {
+    bbmm_status_t st;
+    std::string msg;
+};
+
+#define BBMM_CUDA(x)                                                              \
+    do {                                                                          \
+        cudaError_t e_ = (x);                                                     \
+        if (e_ != cudaSuccess)                                                    \
+            throw ::bbmm::Error{BBMM_ERR_CUDA, std::string(#x) + ": " +           \
+                                                 cudaGetErrorString(e_)};         \
+    } while (0)
+
+#define BBMM_NCCL(x)                                                              \
+    do {                                                                          \
+        ncclResult_t r_ = (x);                                                    \
+        if (r_ != ncclSuccess)                                                    \
+            throw ::bbmm::Error{BBMM_ERR_NCCL, std::string(#x) + ": " +           \
+                                                 ncclGetErrorString(r_)};         \
+    } while (0)
+
+#define BBMM_REQUIRE(cond, msg)                                                   \
+    do {                                                                          \
+        if (!(cond)) throw ::bbmm::Error{BBMM_ERR_ARG, msg};                      \
+    } while (0)
+
+#define BBMM_LAUNCH_CHECK() BBMM_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------- kernel parameters
+// Input-space scaling so the pair kernels evaluate k from a scaled distance:
+//   RBF:    xs = x * sqrt(log2(e)/2) / l   ->  k = s * 2^(-|xs_i - xs_j|^2)
+//   Matern: xs = x * sqrt(5) / l           ->  rh = |xs_i - xs_j| = sqrt5 r,
+//                                              k = s (1 + rh + rh^2/3) e^{-rh}
+struct Hyper {
+    int kind;
+    int n_ls;
+    double ls[kMaxDim];  // lengthscales (host exp of log_ls)
+    double s;            // outputscale
+    double noise_var;    // sigma^2
+    double sigma;
+};
+
+// ------------------------------------------------------------- workspace
+struct Workspace {
+    std::unordered_map<std::string, std::pair<void *, size_t>> bufs;
+    void *get(const std::string &name, size_t bytes);
+    void release_all();
+};
+
+// mBCG device state (one per context; lives in device memory).
+struct MbcgState {
+    int j;                        // current iteration
+    int status;                   // 0 ok, BBMM_ERR_NUMERIC on breakdown
+    int any_active;
+    int pad_;
+    int active[kMaxCols];
+    int iters[kMaxCols];
+    double rho[kMaxCols];         // r^T Phat^{-1} r of the current iterate
+    double rho0[kMaxCols];
+    double bnorm[kMaxCols];
+    double alpha[kMaxCols];       // alpha of the current iteration
+    double beta[kMaxCols];
+    double relres[kMaxCols];
+    double red[4 * kMaxCols];     // reduced sums: [dv | rr | rz | misc]
+};
+
+}  // namespace bbmm
+
+struct bbmm_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int nranks = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    std::string err;
+    bbmm::Workspace ws;
+    int launches = 0;   // library kernel launches since last reset
+};
+
+namespace bbmm {
+
+// --------------------------------------------------------------- helpers
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct RowRange {
+    int64_t r0, r1, nb;
+    int64_t count() const { return r1 > r0 ? r1 - r0 : 0; }
+};
+RowRange local_rows(const bbmm_ctx_s *ctx, int64_t n);
+
+Hyper make_hyper(const bbmm_hyper_t *h, int d);
+
+// ------------------------------------------------ pair kernels (matmul.cu)
+// X scaled for the fp32 pair kernels: n x dp fp32 (dp = padded d).
+int pad_dim(int d);
+int pad_cols(int c);
+void scale_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h,
+                  float *Xs, int dp);
+
+// Kernel-matmul: Vpart[s][i][cp] (fp64) = sum_{j in split s} k(x_{r0+i}, x_j) D32[j][.]
+// (outputscale applied, no sigma^2 term).  Returns number of splits used.
+int kernel_matmul_onthefly(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n,
+                           int64_t r0, int64_t nloc, const float *D32, int cp, double s,
+                           double *Vpart, size_t vpart_cap_elems, cudaEvent_t ev0,
+                           cudaEvent_t ev1);
+int kernel_matmul_stored(bbmm_ctx_s *ctx, const float *Kst, int64_t n, int64_t nloc,
+                         const float *D32, int cp, double *Vpart, size_t vpart_cap_elems,
+                         cudaEvent_t ev0, cudaEvent_t ev1);
+void build_stored_k(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+                    int64_t nloc, double s, float *Kst);
+size_t vpart_elems(int64_t n, int64_t nloc, int cp, bool stored);
+
+// ------------------------------------------------------- pivchol.cu
+void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, int k,
+             double *L, int64_t *piv_h, int *k_used_h, double *resid_h);
+
+// ----------------------------------------------------------- mbcg.cu
+struct MbcgArgs {
+    const float *Xs; int dp; int kind; double s;   // on-the-fly operator
+    const float *Kst;                               // stored operator (or null)
+    int64_t n; int64_t r0; int64_t nloc; int64_t nb;
+    double noise_var;
+    const double *L; int k;                         // k x n (full), k == 0: no precond
+    int c;                                          // columns
+    int max_iter; double tol;
+};
+struct MbcgOut {
+    double *U = nullptr; int64_t ldu = 0;   // optional copy of the solves
+    double *Z0 = nullptr;  // optional: initial Phat^{-1} B (nloc x c), may be null
+    // device-resident results (workspace; valid until the next library call)
+    const double *U_d = nullptr;       // nloc x c solves
+    const double *ahist_d = nullptr;   // max_iter x c
+    const double *bhist_d = nullptr;
+    const MbcgState *state_d = nullptr;
+    std::vector<double> alpha, beta, relres, rho0;
+    std::vector<int> iters;
+    int iters_run = 0;
+    float ms_matmul = 0.f;
+    int matmul_launches = 0;
+};
+void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
+                   double *cholC, double *logdet_d);
+void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
+              const double *cholC, MbcgOut &out);
+void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, int kgen,
+                 int t, const double *L, int k_used, double sigma, int64_t r0, int64_t nloc,
+                 const float *y, double *B, int c);
+
+// -------------------------------------------------------------- slq.cu
+void slq_logdet(bbmm_ctx_s *ctx, const double *alpha_d, const double *beta_d,
+                const int *iters_d, const double *omega_d, int p, int c, int col0, int t,
+                double *out_d, int *status_d);
+
+// ------------------------------------------------------------ deriv.cu
+void derivative_pass(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n,
+                     int64_t r0, int64_t nloc, const float *A32, const float *B32, int cp,
+                     int nq_out, bool ard, int d, double *part, int *nblocks_out);
+size_t derivative_part_elems(int64_t n, int64_t nloc, int dp);
+void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red);
+
+// ------------------------------------------------------------- comm
+void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count);
+void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank);
+
+}  // namespace bbmm

@@ -1,0 +1,620 @@
+// mbcg.cu -- modified batched preconditioned CG (Alg. S2)
+// on the GPU: the per-iteration vector updates, the Woodbury preconditioner
+// apply (App. B, sign-corrected: DESIGN.md R10), the
+// per-column fp64 dot products, and the Lanczos coefficient record
+// (PAPER.md:342-344 / display PAPER.md:468-475).
+//
+// Data layout (local rows of this rank, row-major, fp64):
+//   U, R, Z, D, V : nloc x c        (ld = c)
+//   D32           : n_pad x CS fp32 (all rows; this rank writes rows r0..r1;
+//                                    the all-gather fills the rest)
+//   L             : k x n fp64      (row m = pivoted-Cholesky column m)
+// One iteration j (textbook signs, reading R5/R6):
+//   V = Khat D ; alpha = rho / <D,V> ; U += alpha D ; R -= alpha V ;
+//   relres = |R| / |B| (freeze if < tol) ; S = C^{-1} L^T R ;
+//   Z = (R - L S)/sigma^2 ; rho' = <R,Z> ; beta = rho'/rho ; D = Z + beta D.
+#include <algorithm>
+#include <cmath>
+
+#include "bbmm_internal.cuh"
+
+namespace bbmm {
+
+namespace {
+
+constexpr int kRedBlocks = 2 * kNumSMs;   // persistent reduction grid
+
+// Column-major thread layout for the O(n c) passes: threadIdx.x = column
+// (blockDim.x = CW, a multiple of 32 >= c), threadIdx.y = row within block.
+struct PassGeom {
+    int cw, rb;
+    dim3 block, grid;
+};
+
+PassGeom pass_geom(int64_t nloc, int c) {
+    PassGeom g;
+    g.cw = c <= 32 ? 32 : 64;
+    g.rb = 256 / g.cw;
+    g.block = dim3(g.cw, g.rb);
+    int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, g.rb), kRedBlocks));
+    g.grid = dim3((unsigned)blocks);
+    return g;
+}
+
+// Block-level reduction over threadIdx.y of a per-thread fp64 value for the
+// thread's column, written to part[blockIdx.x * m + col].
+__device__ void block_reduce_cols(double v, double *part, int m, int col_offset) {
+    __shared__ double sred[256];
+    const int tx = threadIdx.x, ty = threadIdx.y, cw = blockDim.x, rb = blockDim.y;
+    sred[ty * cw + tx] = v;
+    __syncthreads();
+    if (ty == 0) {
+        double s = 0.0;
+        for (int y = 0; y < rb; y++) s += sred[y * cw + tx];
+        if (col_offset + tx < m) part[(int64_t)blockIdx.x * m + col_offset + tx] = s;
+    }
+    __syncthreads();
+}
+
+// --------------------------------------------------------------- kernels
+__global__ void k_reduce_blocks(const double *__restrict__ part, int nblk, int m,
+                                double *__restrict__ red) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < m; e += blockDim.x * gridDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nblk; b++) s += part[(int64_t)b * m + e];   // fixed order
+        red[e] = s;
+    }
+}
+
+// R = B, U = 0, D = 0 ; partial sum of B^2 per column.
+__global__ void k_init_vectors(const double *__restrict__ B, int64_t ldb, int64_t nloc, int c,
+                               double *__restrict__ U, double *__restrict__ R,
+                               double *__restrict__ D, double *__restrict__ part) {
+    const int col = threadIdx.x;
+    double acc = 0.0;
+    if (col < c) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
+             i += (int64_t)gridDim.x * blockDim.y) {
+            double b = B[i * ldb + col];
+            R[i * c + col] = b;
+            U[i * c + col] = 0.0;
+            D[i * c + col] = 0.0;
+            acc += b * b;
+        }
+    }
+    block_reduce_cols(acc, part, c, 0);
+}
+
+// W partial = L^T R over this block's rows: part[blk][m*c + col].
+// Thread (col, y): loops over m = y, y + rb, ... (m < k), over the block's rows.
+__global__ void k_LtR(const double *__restrict__ L, int64_t n, int64_t r0, int k,
+                      const double *__restrict__ R, int64_t nloc, int c,
+                      double *__restrict__ part) {
+    const int col = threadIdx.x;
+    const int64_t rows_per_blk = ceil_div(nloc, (int64_t)gridDim.x);
+    const int64_t i0 = (int64_t)blockIdx.x * rows_per_blk;
+    const int64_t i1 = min(nloc, i0 + rows_per_blk);
+    for (int m = threadIdx.y; m < k; m += blockDim.y) {
+        if (col >= c) continue;
+        const double *Lm = L + (int64_t)m * n + r0;
+        double acc = 0.0;
+        for (int64_t i = i0; i < i1; i++) acc += Lm[i] * R[i * c + col];
+        part[(int64_t)blockIdx.x * k * c + (int64_t)m * c + col] = acc;
+    }
+}
+
+// S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One block,
+// thread per column: forward then backward substitution.
+__device__ void chol_solve_col(const double *__restrict__ cholC, int k, const double *W, double *S,
+                               int c, int col) {
+    for (int a = 0; a < k; a++) {
+        double s = W[a * c + col];
+        for (int b = 0; b < a; b++) s -= cholC[a * k + b] * S[b * c + col];
+        S[a * c + col] = s / cholC[a * k + a];
+    }
+    for (int a = k - 1; a >= 0; a--) {
+        double s = S[a * c + col];
+        for (int b = a + 1; b < k; b++) s -= cholC[b * k + a] * S[b * c + col];
+        S[a * c + col] = s / cholC[a * k + a];
+    }
+}
+
+// Z = (R - L S)/sigma^2  (k >= 1) or Z = R (no preconditioner); partial <R,Z>.
+__global__ void k_precond_apply(const double *__restrict__ L, int64_t n, int64_t r0, int k,
+                                const double *__restrict__ S, double noise_var,
+                                const double *__restrict__ R, int64_t nloc, int c,
+                                double *__restrict__ Z, double *__restrict__ part) {
+    extern __shared__ double Ssm[];   // k x c
+    for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < k * c; e += blockDim.x * blockDim.y)
+        Ssm[e] = S[e];
+    __syncthreads();
+    const int col = threadIdx.x;
+    double acc = 0.0;
+    if (col < c) {
+        const double inv = 1.0 / noise_var;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
+             i += (int64_t)gridDim.x * blockDim.y) {
+            double r = R[i * c + col];
+            double z;
+            if (k > 0) {
+                double ls = 0.0;
+                for (int m = 0; m < k; m++) ls += L[(int64_t)m * n + r0 + i] * Ssm[m * c + col];
+                z = (r - ls) * inv;
+            } else {
+                z = r;
+            }
+            Z[i * c + col] = z;
+            acc += r * z;
+        }
+    }
+    block_reduce_cols(acc, part, c, 0);
+}
+
+// Initial state after R = B, Z = P^{-1} B.  red: [bb (c) | rz (c)].
+__global__ void k_init_state(MbcgState *st, const double *__restrict__ bb,
+                             const double *__restrict__ rz, int c) {
+    const int col = threadIdx.x;
+    if (col == 0) { st->j = 0; st->status = 0; st->any_active = 0; }
+    __syncthreads();
+    if (col < c) {
+        double bn = sqrt(bb[col]);
+        st->bnorm[col] = bn;
+        st->rho[col] = rz[col];
+        st->rho0[col] = rz[col];
+        st->active[col] = bn > 0.0;
+        st->iters[col] = 0;
+        st->relres[col] = bn > 0.0 ? 1.0 : 0.0;
+        st->alpha[col] = 0.0;
+        st->beta[col] = 0.0;
+        if (bn > 0.0) atomicOr(&st->any_active, 1);
+    }
+}
+
+// Pass A: V = sum_s Vpart[s] + sigma^2 D ; partial <D, V>.
+__global__ void k_passA(const double *__restrict__ Vpart, int splits, int cs, int64_t nloc, int c,
+                        double noise_var, const double *__restrict__ D, double *__restrict__ V,
+                        double *__restrict__ part) {
+    const int col = threadIdx.x;
+    double acc = 0.0;
+    if (col < c) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
+             i += (int64_t)gridDim.x * blockDim.y) {
+            double v = 0.0;
+            for (int s = 0; s < splits; s++) v += Vpart[((int64_t)s * nloc + i) * cs + col];
+            double dv = D[i * c + col];
+            v += noise_var * dv;
+            V[i * c + col] = v;
+            acc += dv * v;
+        }
+    }
+    block_reduce_cols(acc, part, c, 0);
+}
+
+// alpha = rho / <D,V> for active columns; record alpha_j; breakdown check.
+__global__ void k_alpha(MbcgState *st, const double *__restrict__ dv, double *__restrict__ ahist,
+                        int c) {
+    const int col = threadIdx.x;
+    if (col >= c) return;
+    const int j = st->j;
+    double a = 0.0;
+    if (st->active[col]) {
+        a = st->rho[col] / dv[col];
+        if (!(a > 0.0) || !isfinite(a)) {   // indefinite operator (reading R24)
+            st->status = BBMM_ERR_NUMERIC;
+            a = 0.0;
+            st->active[col] = 0;
+        } else {
+            ahist[(int64_t)j * c + col] = a;
+            st->iters[col] = j + 1;
+        }
+    }
+    st->alpha[col] = a;
+}
+
+// Pass B: U += alpha D ; R -= alpha V ; partial |R|^2.
+__global__ void k_passB(const MbcgState *__restrict__ st, const double *__restrict__ D,
+                        const double *__restrict__ V, int64_t nloc, int c, double *__restrict__ U,
+                        double *__restrict__ R, double *__restrict__ part) {
+    const int col = threadIdx.x;
+    double acc = 0.0;
+    if (col < c) {
+        const double a = st->alpha[col];
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
+             i += (int64_t)gridDim.x * blockDim.y) {
+            double r = R[i * c + col];
+            if (a != 0.0) {
+                U[i * c + col] += a * D[i * c + col];
+                r -= a * V[i * c + col];
+                R[i * c + col] = r;
+            }
+            acc += r * r;
+        }
+    }
+    block_reduce_cols(acc, part, c, 0);
+}
+
+// relres, freezing (relres < tol, reading R9), then S = C^{-1} W.
+// red layout: [rr (c) | W (k*c)].
+__global__ void k_after_B(MbcgState *st, const double *__restrict__ red, const double *cholC,
+                          int k, int c, double tol, double *__restrict__ S) {
+    const int col = threadIdx.x;
+    if (col >= c) return;
+    if (st->active[col]) {
+        double rel = sqrt(red[col]) / st->bnorm[col];
+        st->relres[col] = rel;
+        if (rel < tol) st->active[col] = 0;
+    }
+    if (k > 0) chol_solve_col(cholC, k, red + c, S, c, col);
+}
+
+// S = C^{-1} W at initialisation (red = W).
+__global__ void k_solve_S(const double *__restrict__ W, const double *cholC, int k, int c,
+                          double *__restrict__ S) {
+    const int col = threadIdx.x;
+    if (col < c && k > 0) chol_solve_col(cholC, k, W, S, c, col);
+}
+
+// beta = rho'/rho ; record beta_j ; rho = rho' ; exact convergence freezes.
+__global__ void k_beta(MbcgState *st, const double *__restrict__ rz, double *__restrict__ bhist,
+                       int c) {
+    const int col = threadIdx.x;
+    __shared__ int any;
+    if (col == 0) any = 0;
+    __syncthreads();
+    if (col < c) {
+        const int j = st->j;
+        double b = 0.0;
+        if (st->active[col]) {
+            double r = rz[col];
+            if (r == 0.0) {
+                st->active[col] = 0;   // R = 0 exactly
+            } else {
+                b = r / st->rho[col];
+                st->rho[col] = r;
+                bhist[(int64_t)j * c + col] = b;
+            }
+        }
+        st->beta[col] = b;
+        if (st->active[col]) atomicOr(&any, 1);
+    }
+    __syncthreads();
+    if (col == 0) st->any_active = any;
+}
+
+// Pass D: D = Z + beta D (active), 0 (frozen); D32 rows r0.. (fp32, stride cs);
+// block 0 advances the iteration counter.
+__global__ void k_passD(MbcgState *st, const double *__restrict__ Z, int64_t nloc, int c,
+                        int64_t r0, int cs, double *__restrict__ D, float *__restrict__ D32,
+                        int advance) {
+    const int col = threadIdx.x;
+    if (col < cs) {
+        const bool act = col < c && st->active[col];
+        const double b = col < c ? st->beta[col] : 0.0;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
+             i += (int64_t)gridDim.x * blockDim.y) {
+            double dn = 0.0;
+            if (act) dn = Z[i * c + col] + b * D[i * c + col];
+            if (col < c) D[i * c + col] = dn;
+            D32[(r0 + i) * cs + col] = (float)dn;
+        }
+    }
+    if (advance && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+        // every thread of every block has read st->beta/active before any
+        // kernel that follows in stream order; j is only read by later kernels
+        st->j += 1;
+    }
+}
+
+__global__ void k_copy(const double *__restrict__ a, double *__restrict__ b, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
+__global__ void k_copy_U(const double *__restrict__ U, int64_t nloc, int c, double *__restrict__ out,
+                         int64_t ldo) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * c;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / c;
+        out[i * ldo + (e - i * c)] = U[e];
+    }
+}
+
+// ------------------------------------------------- preconditioner setup
+// C = sigma^2 I + L^T L (k x k) over all n rows, block partials.
+__global__ void k_LtL(const double *__restrict__ L, int64_t n, int k, double *__restrict__ part) {
+    const int64_t rows_per_blk = ceil_div(n, (int64_t)gridDim.x);
+    const int64_t i0 = (int64_t)blockIdx.x * rows_per_blk;
+    const int64_t i1 = min(n, i0 + rows_per_blk);
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        int a = e / k, b = e - a * k;
+        if (b > a) continue;
+        const double *La = L + (int64_t)a * n, *Lb = L + (int64_t)b * n;
+        double acc = 0.0;
+        for (int64_t i = i0; i < i1; i++) acc += La[i] * Lb[i];
+        part[(int64_t)blockIdx.x * k * k + e] = acc;
+    }
+}
+
+// In-place Cholesky of C (k x k, lower) + log|P| = log|C| + (n-k) log sigma^2.
+__global__ void k_chol_small(double *C, const double *__restrict__ red, int k, double noise_var,
+                             int64_t n, double *logdet, int *status) {
+    // single thread: k <= 128, O(k^3/3) = 0.7 MFLOP
+    if (threadIdx.x != 0) return;
+    for (int a = 0; a < k; a++)
+        for (int b = 0; b <= a; b++) {
+            double v = red[a * k + b] + (a == b ? noise_var : 0.0);
+            C[a * k + b] = v;
+            C[b * k + a] = v;
+        }
+    for (int jj = 0; jj < k; jj++) {
+        double s = C[jj * k + jj];
+        for (int m = 0; m < jj; m++) s -= C[jj * k + m] * C[jj * k + m];
+        if (!(s > 0.0)) { *status = BBMM_ERR_NUMERIC; return; }
+        double l = sqrt(s);
+        C[jj * k + jj] = l;
+        for (int i = jj + 1; i < k; i++) {
+            double t = C[i * k + jj];
+            for (int m = 0; m < jj; m++) t -= C[i * k + m] * C[jj * k + m];
+            C[i * k + jj] = t / l;
+        }
+        for (int i = 0; i < jj; i++) C[i * k + jj] = 0.0;
+    }
+    double ld = 0.0;
+    for (int a = 0; a < k; a++) ld += 2.0 * log(C[a * k + a]);
+    *logdet = ld + (double)(n - k) * log(noise_var);
+}
+
+// ------------------------------------------------------------ probes
+// Counter-based splitmix64 Rademacher signs.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double rsign(uint64_t seed, int64_t n, int kgen, int col, int64_t row) {
+    uint64_t ctr = (uint64_t)col * (uint64_t)(n + kgen) + (uint64_t)row + 1ULL;
+    return (mix64(seed + ctr * 0x9E3779B97F4A7C15ULL) >> 63) ? -1.0 : 1.0;
+}
+
+// B[i][0] = y_{r0+i} ; B[i][1+col] = sum_m L[m][r0+i] eps1[m][col] + sig eps2[r0+i][col]
+__global__ void k_probes(const int8_t *__restrict__ eps, uint64_t seed, int64_t n, int kgen, int t,
+                         const double *__restrict__ L, int k_used, double sig, int64_t r0,
+                         int64_t nloc, const float *__restrict__ y, double *__restrict__ B) {
+    const int c = t + 1;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * c;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = e / c;
+        int col = (int)(e - i * c);
+        int64_t gi = r0 + i;
+        double v;
+        if (col == 0) {
+            v = (double)y[gi];
+        } else {
+            int pc = col - 1;
+            double acc = 0.0;
+            for (int m = 0; m < k_used; m++) {
+                double e1 = eps ? (double)eps[(n + m) * t + pc] : rsign(seed, n, kgen, pc, n + m);
+                acc += L[(int64_t)m * n + gi] * e1;
+            }
+            double e2 = eps ? (double)eps[gi * t + pc] : rsign(seed, n, kgen, pc, gi);
+            v = acc + sig * e2;
+        }
+        B[e] = v;
+    }
+}
+
+}  // namespace
+
+// ======================================================================
+// host side
+// ======================================================================
+void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red) {
+    k_reduce_blocks<<<std::max(1, (int)ceil_div(m, 256)), 256, 0, ctx->stream>>>(part, nblk, m,
+                                                                                red);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
+                   double *cholC, double *logdet_d) {
+    int *status = (int *)ctx->ws.get("pc_status", sizeof(int));
+    BBMM_CUDA(cudaMemsetAsync(status, 0, sizeof(int), ctx->stream));
+    if (k == 0) {
+        BBMM_CUDA(cudaMemsetAsync(logdet_d, 0, sizeof(double), ctx->stream));
+        return;
+    }
+    int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRedBlocks, ceil_div(n, 1024)));
+    double *part = (double *)ctx->ws.get("pc_part", sizeof(double) * nblk * k * k);
+    double *red = (double *)ctx->ws.get("pc_red", sizeof(double) * k * k);
+    k_LtL<<<nblk, 256, 0, ctx->stream>>>(L, n, k, part);
+    k_reduce_blocks<<<ceil_div(k * k, 256), 256, 0, ctx->stream>>>(part, nblk, k * k, red);
+    k_chol_small<<<1, 32, 0, ctx->stream>>>(cholC, red, k, noise_var, n, logdet_d, status);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches += 3;
+    int st_h = 0;
+    BBMM_CUDA(cudaMemcpyAsync(&st_h, status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (st_h != 0) throw Error{BBMM_ERR_NUMERIC, "Cholesky of C = sigma^2 I + L^T L failed"};
+}
+
+void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, int kgen, int t,
+                 const double *L, int k_used, double sigma, int64_t r0, int64_t nloc,
+                 const float *y, double *B, int c) {
+    (void)c;
+    int64_t total = nloc * (t + 1);
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
+    k_probes<<<grid, 256, 0, ctx->stream>>>(eps, seed, n, kgen, t, L, k_used, sigma, r0, nloc, y,
+                                            B);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
+              const double *cholC, MbcgOut &out) {
+    const int c = a.c, k = a.k;
+    const int cp = pad_cols(c);
+    BBMM_REQUIRE(cp > 0, "too many columns");
+    const int cs = (cp + 3) & ~3;
+    const int64_t nloc = a.nloc;
+    const size_t nc = (size_t)std::max<int64_t>(nloc, 1) * c;
+    Workspace &ws = ctx->ws;
+    cudaStream_t sm = ctx->stream;
+
+    double *U = (double *)ws.get("cg_U", nc * 8);
+    double *R = (double *)ws.get("cg_R", nc * 8);
+    double *Z = (double *)ws.get("cg_Z", nc * 8);
+    double *D = (double *)ws.get("cg_D", nc * 8);
+    double *V = (double *)ws.get("cg_V", nc * 8);
+    const int64_t npad = a.nb * ctx->nranks;
+    float *D32 = (float *)ws.get("cg_D32", (size_t)npad * cs * 4);
+    size_t vcap = vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
+    double *Vpart = (double *)ws.get("cg_Vpart", std::max<size_t>(vcap, 1) * 8);
+    const PassGeom g = pass_geom(nloc, c);
+    const int nblk = (int)g.grid.x;
+    const int kk = std::max(k, 1);
+    double *part = (double *)ws.get("cg_part", (size_t)nblk * (size_t)(kk + 1) * c * 8);
+    double *red = (double *)ws.get("cg_red", (size_t)(kk + 2) * c * 8);
+    double *S = (double *)ws.get("cg_S", (size_t)kk * c * 8);
+    MbcgState *st = (MbcgState *)ws.get("cg_state", sizeof(MbcgState));
+    double *ahist = (double *)ws.get("cg_ahist", (size_t)a.max_iter * c * 8);
+    double *bhist = (double *)ws.get("cg_bhist", (size_t)a.max_iter * c * 8);
+    BBMM_CUDA(cudaMemsetAsync(ahist, 0, (size_t)a.max_iter * c * 8, sm));
+    BBMM_CUDA(cudaMemsetAsync(bhist, 0, (size_t)a.max_iter * c * 8, sm));
+    BBMM_CUDA(cudaMemsetAsync(D32, 0, (size_t)npad * cs * 4, sm));
+    const size_t smem_S = (size_t)kk * c * 8;
+    if (smem_S > 48 * 1024)
+        BBMM_CUDA(cudaFuncSetAttribute(k_precond_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_S));
+    const bool multi = ctx->nranks > 1;
+    int launches = 0;
+
+    auto reduce = [&](int m, double *dst) {
+        k_reduce_blocks<<<std::max(1, (int)ceil_div(m, 256)), 256, 0, sm>>>(part, nblk, m, dst);
+        launches++;
+    };
+    // W = L^T R (+ |R|^2 already in red[0..c) when with_rr) -> red[c..c+kc)
+    auto LtR = [&](double *dst) {
+        if (k == 0) return;
+        k_LtR<<<g.grid, g.block, 0, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part);
+        reduce(k * c, dst);
+        launches++;
+    };
+
+    // ---------------- initialisation: R = B, Z = P^{-1} R, D = Z
+    k_init_vectors<<<g.grid, g.block, 0, sm>>>(B, ldb, nloc, c, U, R, D, part);
+    launches++;
+    reduce(c, red);                           // red[0..c) = |B|^2
+    LtR(red + c);                             // red[c..c+kc) = L^T B
+    if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
+    if (k > 0) {
+        k_solve_S<<<1, 64, 0, sm>>>(red + c, cholC, k, c, S);
+        launches++;
+    }
+    double *red_rz = red + (size_t)(kk + 1) * c;
+    k_precond_apply<<<g.grid, g.block, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R, nloc, c,
+                                                     Z, part);
+    launches++;
+    reduce(c, red_rz);
+    if (multi) allreduce_sum(ctx, red_rz, c);
+    k_init_state<<<1, 64, 0, sm>>>(st, red, red_rz, c);
+    launches++;
+    if (out.Z0) {
+        k_copy<<<256, 256, 0, sm>>>(Z, out.Z0, (int64_t)nc);
+        launches++;
+    }
+    k_passD<<<g.grid, dim3(cs <= 32 ? 32 : 64, g.rb), 0, sm>>>(st, Z, nloc, c, a.r0, cs, D, D32, 0);
+    launches++;
+    if (multi) allgather_rows(ctx, D32, (size_t)a.nb * cs * 4);
+    BBMM_LAUNCH_CHECK();
+
+    // ---------------- iterations
+    cudaEvent_t ev0, ev1;
+    BBMM_CUDA(cudaEventCreate(&ev0));
+    BBMM_CUDA(cudaEventCreate(&ev1));
+    std::vector<cudaEvent_t> mm_ev;
+    int *any_h = nullptr;
+    BBMM_CUDA(cudaMallocHost(&any_h, sizeof(int)));
+    int iters_run = 0;
+    for (int j = 0; j < a.max_iter; j++) {
+        cudaEvent_t e0, e1;
+        BBMM_CUDA(cudaEventCreate(&e0));
+        BBMM_CUDA(cudaEventCreate(&e1));
+        mm_ev.push_back(e0);
+        mm_ev.push_back(e1);
+        int splits;
+        if (a.Kst)
+            splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, D32, cp, Vpart, vcap, e0, e1);
+        else
+            splits = kernel_matmul_onthefly(ctx, a.kind, a.Xs, a.dp, a.n, a.r0, nloc, D32, cp, a.s,
+                                            Vpart, vcap, e0, e1);
+        k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
+        reduce(c, red);
+        if (multi) allreduce_sum(ctx, red, c);
+        k_alpha<<<1, 64, 0, sm>>>(st, red, ahist, c);
+        k_passB<<<g.grid, g.block, 0, sm>>>(st, D, V, nloc, c, U, R, part);
+        reduce(c, red);
+        LtR(red + c);
+        if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
+        k_after_B<<<1, 64, 0, sm>>>(st, red, cholC, k, c, a.tol, S);
+        k_precond_apply<<<g.grid, g.block, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R,
+                                                         nloc, c, Z, part);
+        reduce(c, red_rz);
+        if (multi) allreduce_sum(ctx, red_rz, c);
+        k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
+        k_passD<<<g.grid, dim3(cs <= 32 ? 32 : 64, g.rb), 0, sm>>>(st, Z, nloc, c, a.r0, cs, D,
+                                                                    D32, 1);
+        launches += 8;
+        if (multi) allgather_rows(ctx, D32, (size_t)a.nb * cs * 4);
+        BBMM_LAUNCH_CHECK();
+        iters_run = j + 1;
+        if (a.tol > 0.0) {
+            BBMM_CUDA(cudaMemcpyAsync(any_h, &st->any_active, sizeof(int), cudaMemcpyDeviceToHost,
+                                      sm));
+            BBMM_CUDA(cudaStreamSynchronize(sm));
+            if (!*any_h) break;
+        }
+    }
+    // ---------------- outputs
+    if (out.U) {
+        k_copy_U<<<256, 256, 0, sm>>>(U, nloc, c, out.U, out.ldu);
+        launches++;
+    }
+    MbcgState st_h;
+    out.alpha.assign((size_t)a.max_iter * c, 0.0);
+    out.beta.assign((size_t)a.max_iter * c, 0.0);
+    BBMM_CUDA(cudaMemcpyAsync(out.alpha.data(), ahist, (size_t)a.max_iter * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaMemcpyAsync(out.beta.data(), bhist, (size_t)a.max_iter * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaMemcpyAsync(&st_h, st, sizeof(MbcgState), cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaStreamSynchronize(sm));
+    BBMM_LAUNCH_CHECK();
+    float ms_tot = 0.f;
+    for (size_t q = 0; q + 1 < mm_ev.size(); q += 2) {
+        float ms = 0.f;
+        BBMM_CUDA(cudaEventElapsedTime(&ms, mm_ev[q], mm_ev[q + 1]));
+        ms_tot += ms;
+        cudaEventDestroy(mm_ev[q]);
+        cudaEventDestroy(mm_ev[q + 1]);
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    cudaFreeHost(any_h);
+    out.ms_matmul = ms_tot;
+    out.matmul_launches = iters_run;
+    out.iters_run = iters_run;
+    out.U_d = U;
+    out.ahist_d = ahist;
+    out.bhist_d = bhist;
+    out.state_d = st;
+    out.iters.assign(st_h.iters, st_h.iters + c);
+    out.relres.assign(st_h.relres, st_h.relres + c);
+    out.rho0.assign(st_h.rho0, st_h.rho0 + c);
+    ctx->launches += launches;   // matmul launches are counted by the matmul functions
+    if (st_h.status != 0)
+        throw Error{BBMM_ERR_NUMERIC,
+                    "mBCG breakdown: alpha <= 0 or non-finite (operator not positive definite)"};
+}
+
+}  // namespace bbmm

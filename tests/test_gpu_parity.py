@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same
+seeded inputs.  Tolerances: solves <= 1e-4 per
+column (norm-wise), log-det / MLL <= 1e-3 relative, gradient <= 1e-3
+norm-wise, pivots bit-exact; a single Khat*D matmul is held to its fp32
+summation bound."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_1809_11165_b200 as bb  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = bb.Context(0)
+    yield c
+    c.close()
+
+
+def hyper_of(pr):
+    return bb.Hyper(pr.cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
+
+
+def dev(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def colwise_rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b, axis=0) / np.maximum(np.linalg.norm(b, axis=0), 1e-300)
+
+
+# ------------------------------------------------------------ kernel matmul
+MATMUL_CASES = [
+    ("C0", 256, 11), ("C0", 1000, 5), ("C1", 3338, 11), ("C2", 2777, 17), ("C3", 3001, 33),
+    ("C4", 4099, 17), ("C4", 70, 1), ("C2", 513, 64),
+]
+
+
+@pytest.mark.parametrize("name,n,c", MATMUL_CASES)
+@pytest.mark.parametrize("kmode", [bb.ONTHEFLY, bb.STORED])
+def test_kernel_matmul_matches_oracle(ctx, orc, name, n, c, kmode):
+    pr = synth.make_problem(synth.scaled(synth.CONFIGS[name], n), seed=3)
+    D = synth.random_block(n, c, seed=4).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), kmode).cpu().numpy()
+    ref = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
+    # summation bound: |err_i| <= tol * (K|D| + sigma^2 |D|)_i  (K >= 0)
+    absb = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D))
+    err = np.abs(V - ref)
+    assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
+    assert colwise_rel(V, ref).max() < 2e-5
+
+
+# ------------------------------------------------------------ pivoted Cholesky
+@pytest.mark.parametrize("name,n", [("C0", 256), ("C1", 3338), ("C2", 5000), ("C3", 4000),
+                                    ("C4", 20000)])
+def test_pivchol_pivots_bit_exact(ctx, orc, name, n):
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=0)
+    L, piv, ku, res = bb.pivchol(ctx, dev(pr.X), hyper_of(pr), cfg.k)
+    Lo, pivo, kuo, reso = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, cfg.k)
+    assert ku == kuo
+    np.testing.assert_array_equal(piv, pivo)
+    np.testing.assert_allclose(L.cpu().numpy().T, Lo, rtol=1e-9, atol=1e-12)
+    assert res == pytest.approx(reso, rel=1e-9, abs=1e-9)
+
+
+def test_pivchol_early_stop_at_numerical_rank(ctx, orc):
+    """1-D points on a coarse grid with a huge lengthscale: rank collapses (reading R23)."""
+    X = np.repeat(np.linspace(0, 1, 5, dtype=np.float32), 8)[:, None]
+    h = bb.Hyper(bb.RBF, np.array([0.0]), 0.0, math.log(0.1))
+    L, piv, ku, res = bb.pivchol(ctx, dev(X), h, 12)
+    Lo, pivo, kuo, reso = orc.pivchol_kernel(0, X, [0.0], 0.0, 12)
+    assert ku == kuo and ku < 12
+    np.testing.assert_array_equal(piv, pivo)
+
+
+# ------------------------------------------------------------------- mBCG
+@pytest.mark.parametrize("name,n,k", [("C0", 256, 5), ("C1", 1500, 5), ("C4", 3000, 30),
+                                      ("C2", 1200, 0)])
+def test_mbcg_matches_oracle(ctx, orc, name, n, k):
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=1)
+    c = cfg.t + 1
+    B = synth.random_block(n, c, seed=5).astype(np.float64)
+    Lo = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, k)[0] if k else None
+    Ld = dev(Lo.T, torch.float64) if k else None
+    r = bb.mbcg(ctx, dev(pr.X), hyper_of(pr), dev(B, torch.float64), L=Ld, max_iter=cfg.p)
+    ro = orc.mbcg_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, B, cfg.p, L=Lo)
+    np.testing.assert_array_equal(r["iters"], ro["iters"])
+    assert colwise_rel(r["U"].cpu().numpy(), ro["U"]).max() < 1e-4
+    np.testing.assert_allclose(r["alpha"], ro["alpha"], rtol=1e-3)
+    np.testing.assert_allclose(r["rho0"], ro["rho0"], rtol=1e-12)
+
+
+def test_mbcg_tolerance_freezes_columns(ctx, orc):
+    cfg = synth.scaled(synth.CONFIGS["C1"], 800)
+    pr = synth.make_problem(cfg, seed=2)
+    B = synth.random_block(800, 4, seed=6).astype(np.float64)
+    Lo = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, 5)[0]
+    r = bb.mbcg(ctx, dev(pr.X), hyper_of(pr), dev(B, torch.float64), L=dev(Lo.T, torch.float64),
+                max_iter=50, tol=1e-3)
+    ro = orc.mbcg_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, B, 50, tol=1e-3, L=Lo)
+    np.testing.assert_array_equal(r["iters"], ro["iters"])
+    assert np.all(r["relres"] < 1e-3)
+    assert colwise_rel(r["U"].cpu().numpy(), ro["U"]).max() < 1e-4
+
+
+# -------------------------------------------------------- MLL + gradient
+MLL_CASES = [("C0", 256), ("C1", 3338), ("C2", 3000), ("C3", 2500), ("C4", 4000), ("C4", 1001)]
+
+
+def run_both(ctx, orc, cfg, seed=0, kmode=None, k=None, t=None):
+    pr = synth.make_problem(cfg, seed=seed)
+    k = cfg.k if k is None else k
+    t = cfg.t if t is None else t
+    km = (bb.STORED if cfg.stored else bb.ONTHEFLY) if kmode is None else kmode
+    g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), t, k, cfg.p, seed=7, kmode=km,
+                        return_solves=True)
+    o = orc.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, t, k, cfg.p,
+                         seed=7)
+    return pr, g, o
+
+
+@pytest.mark.parametrize("name,n", MLL_CASES)
+def test_mll_and_grad_matches_oracle(ctx, orc, name, n):
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr, g, o = run_both(ctx, orc, cfg)
+    st = g["stats"]
+    np.testing.assert_array_equal(g["pivots"], o["pivots"])
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+    assert abs(st["logdet"] - o["logdet"]) <= 1e-3 * abs(o["logdet"])
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
+    assert st["k_used"] == o["k_used"]
+
+
+@pytest.mark.parametrize("kmode", [bb.ONTHEFLY, bb.STORED])
+def test_stored_and_onthefly_agree(ctx, orc, kmode):
+    cfg = synth.scaled(synth.CONFIGS["C2"], 2048)
+    pr, g, o = run_both(ctx, orc, cfg, kmode=kmode)
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+
+
+@pytest.mark.parametrize("k,t", [(0, 10), (5, 1), (40, 3)])
+def test_edge_ranks_and_probe_counts(ctx, orc, k, t):
+    cfg = synth.scaled(synth.CONFIGS["C0"], 256)
+    pr, g, o = run_both(ctx, orc, cfg, k=k, t=t)
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
+
+
+def test_tiny_problem(ctx, orc):
+    cfg = synth.scaled(synth.CONFIGS["C4"], 7)
+    cfg = synth.dataclasses.replace(cfg, k=3, t=2, p=7)
+    pr, g, o = run_both(ctx, orc, cfg)
+    assert g["mll"] == pytest.approx(o["mll"], rel=1e-6)
+    np.testing.assert_allclose(g["grad"], o["grad"], rtol=1e-4, atol=1e-8)
+
+
+def test_explicit_eps_matches_generator(ctx, orc):
+    cfg = synth.scaled(synth.CONFIGS["C0"], 256)
+    pr = synth.make_problem(cfg)
+    eps = orc.rademacher(7, 256, cfg.k, cfg.t)
+    a = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), cfg.t, cfg.k, cfg.p, seed=7)
+    b = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), cfg.t, cfg.k, cfg.p, seed=999,
+                        eps=dev(eps, torch.int8))
+    assert a["mll"] == b["mll"]
+    np.testing.assert_array_equal(a["grad"], b["grad"])
+
+
+def test_errors_are_reported(ctx):
+    X = dev(np.zeros((10, 2), np.float32))
+    y = dev(np.zeros(10, np.float32))
+    h = bb.Hyper(bb.RBF, np.array([0.0]), 0.0, 0.0)
+    with pytest.raises(bb.BBMMError) as e:
+        bb.mll_and_grad(ctx, X, y, h, t=0, k=2)
+    assert e.value.status == 2
+    Xn = X.clone()
+    Xn[3, 1] = float("nan")
+    with pytest.raises(bb.BBMMError) as e:
+        bb.mll_and_grad(ctx, Xn, y, h, t=2, k=2)
+    assert e.value.status == 3
+    with pytest.raises(bb.BBMMError) as e:
+        bb.mll_and_grad(ctx, X, y, bb.Hyper(bb.RBF, np.array([0.0, 0.0, 0.0]), 0.0, 0.0), t=2, k=2)
+    assert e.value.status == 2
+
+
+# ---------------------------------------------- full-size sampled parity
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_matmul_sampled_rows(ctx, orc, name):
+    """BASELINE sizes, launch configuration of the bench: sampled rows vs oracle."""
+    cfg = synth.CONFIGS[name]
+    pr = synth.make_problem(cfg, seed=0)
+    c = cfg.t + 1
+    D = synth.random_block(cfg.n, c, seed=4).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr)).cpu().numpy()
+    rows = np.unique(np.concatenate([[0, 1, cfg.n - 1], np.random.default_rng(0).integers(0, cfg.n, 29)]))
+    ref = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D, rows=rows)
+    absb = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D), rows=rows)
+    err = np.abs(V[rows] - ref)
+    assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
+
+
+@pytest.mark.slow
+def test_full_size_pivchol_c4_bit_exact(ctx, orc):
+    cfg = synth.CONFIGS["C4"]
+    pr = synth.make_problem(cfg, seed=0)
+    L, piv, ku, res = bb.pivchol(ctx, dev(pr.X), hyper_of(pr), cfg.k)
+    _, pivo, kuo, reso = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, cfg.k)
+    assert ku == kuo
+    np.testing.assert_array_equal(piv, pivo)
