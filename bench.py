@@ -142,6 +142,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kmode", default=None, choices=[None, "onthefly", "stored"])
+    ap.add_argument("--precision", default="fp64acc", choices=["fp64acc", "fp32acc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -166,6 +167,7 @@ def main():
     kmode = {"onthefly": bb.ONTHEFLY, "stored": bb.STORED}.get(
         args.kmode, bb.STORED if cfg.stored else bb.ONTHEFLY)
     ctx = bb.Context(local_rank)
+    ctx.set_matmul_precision(bb.FP64ACC if args.precision == "fp64acc" else bb.FP32ACC)
     if world > 1:
         ctx.set_comm()
     X = torch.from_numpy(pr.X).cuda()
@@ -275,6 +277,7 @@ def main():
                                f"k={cfg.k}, p={cfg.p}, "
                                f"{'stored' if kmode == bb.STORED else 'on-the-fly'} K",
                    "parallelism": f"row-partition x{world}",
+                   "matmul_precision": args.precision,
                    "l2": "256 MB L2 flush between timed steps"},
         "roofline": roofline, "e2e": e2e, "gpu_launches": launches // max(len(stats), 1) * args.steps,
         "clocks": clocks,

@@ -67,6 +67,16 @@ typedef enum { BBMM_RBF = 0, BBMM_MATERN52 = 1 } bbmm_kernel_t;
  * call and streams it from HBM every iteration. */
 typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
 
+/* Arithmetic of the blackbox matmul Khat*D.
+ * FP64ACC (default): kernel values in fp32 (MUFU ex2/sqrt), search directions
+ *   D in fp64, products and sums in fp64.  Parity with the fp64 oracle holds
+ *   whether or not mBCG has converged by max_iter (a per-iteration fp32
+ *   rounding of D is amplified by an unconverged Krylov process).
+ * FP32ACC: D rounded to fp32, products summed in fp32 over 16 terms then
+ *   folded into fp64.  Faster; parity holds only where mBCG has converged
+ *   (SURVEY.md §8c "regime A"). */
+typedef enum { BBMM_MATMUL_FP64ACC = 0, BBMM_MATMUL_FP32ACC = 1 } bbmm_matmul_precision_t;
+
 typedef struct {
     int32_t kind;            /* bbmm_kernel_t */
     int32_t n_ls;            /* 1 (isotropic) or d (ARD) */
@@ -112,6 +122,8 @@ const char *bbmm_version(void);
 bbmm_status_t bbmm_nccl_unique_id(void *out_128_bytes);
 bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank,
                                 const void *nccl_unique_id_128_bytes);
+/* Select the matmul arithmetic for subsequent calls on ctx (default FP64ACC). */
+bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p);
 /* Local row range [*r0, *r1) of this rank for problem size n. */
 bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0,
                               int64_t *r1);

@@ -24,6 +24,8 @@ RBF = 0
 MATERN52 = 1
 ONTHEFLY = 0
 STORED = 1
+FP64ACC = 0     # matmul precision (default): fp64 D, fp64 products and sums
+FP32ACC = 1     # fp32 D, 16-term fp32 chunks folded into fp64 (regime A only)
 
 _STATUS = {0: "OK", 2: "ERR_ARG", 3: "ERR_DATA", 4: "ERR_NUMERIC", 5: "ERR_CUDA",
            6: "ERR_NCCL", 7: "ERR_OOM"}
@@ -69,6 +71,7 @@ _lib.bbmm_ctx_create.argtypes = [C.c_int, _p, C.POINTER(_p)]
 _lib.bbmm_ctx_destroy.argtypes = [_p]
 _lib.bbmm_nccl_unique_id.argtypes = [_p]
 _lib.bbmm_ctx_set_comm.argtypes = [_p, C.c_int, C.c_int, _p]
+_lib.bbmm_ctx_set_matmul_precision.argtypes = [_p, C.c_int]
 _lib.bbmm_local_rows.argtypes = [_p, _i64, C.POINTER(_i64), C.POINTER(_i64)]
 _lib.bbmm_kernel_matmul.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _i64, _p, _i64]
 _lib.bbmm_pivchol.argtypes = [_p, _p, _i64, _i32, _HP, _i32, _p, _p, C.POINTER(_i32),
@@ -78,7 +81,7 @@ _lib.bbmm_mbcg.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _p, _i32,
 _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d,
                                    _u64, _p, C.POINTER(_d), _p, C.POINTER(Stats), _p, _p]
 for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
-           "bbmm_local_rows", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
+           "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
            "bbmm_mll_and_grad"):
     getattr(_lib, _f).restype = C.c_int
 
@@ -161,6 +164,10 @@ class Context:
         raw = (C.c_char * 128).from_buffer_copy(obj[0])
         self.check(_lib.bbmm_ctx_set_comm(self._h, ws, rk, C.cast(raw, _p)))
         self.nranks, self.rank = ws, rk
+        return self
+
+    def set_matmul_precision(self, prec: int):
+        self.check(_lib.bbmm_ctx_set_matmul_precision(self._h, int(prec)))
         return self
 
     def local_rows(self, n):

@@ -78,15 +78,16 @@ void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank) {
 
 namespace {
 
-// D (fp64, rows [r0, r0+rows) of an n x c block, ld) -> D32 rows at the same
-// global positions, fp32, stride cs (zero padding columns).
-__global__ void k_pack_d32(const double *__restrict__ D, int64_t ldd, int64_t rows, int c,
-                           int64_t row_off, int cs, float *__restrict__ D32) {
+// D (fp64, rows [0, rows) of an n x c block, ld) -> the matmul operand Dm
+// (fp64 or fp32, stride cs, zero padding columns).
+template <typename DT>
+__global__ void k_pack_dm(const double *__restrict__ D, int64_t ldd, int64_t rows, int c, int cs,
+                          DT *__restrict__ Dm) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cs;
          e += (int64_t)gridDim.x * blockDim.x) {
         int64_t i = e / cs;
         int col = (int)(e - i * cs);
-        D32[(row_off + i) * cs + col] = col < c ? (float)D[i * ldd + col] : 0.0f;
+        Dm[i * cs + col] = col < c ? (DT)D[i * ldd + col] : DT(0);
     }
 }
 
@@ -280,6 +281,12 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
     });
 }
 
+bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p) {
+    if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC)) return BBMM_ERR_ARG;
+    ctx->matmul_acc64 = (p == BBMM_MATMUL_FP64ACC);
+    return BBMM_OK;
+}
+
 bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0, int64_t *r1) {
     if (!ctx || !r0 || !r1 || n < 0) return BBMM_ERR_ARG;
     RowRange rr = local_rows(ctx, n);
@@ -303,8 +310,14 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
         const int dp = pad_dim(d), cp = pad_cols(ncols), cs = (cp + 3) & ~3, ds = (dp + 3) & ~3;
         float *Xs = (float *)ctx->ws.get("Xs", (size_t)n * ds * 4);
         scale_inputs(ctx, X, n, d, h, Xs, dp);
-        float *D32 = (float *)ctx->ws.get("mm_D32", (size_t)n * cs * 4);
-        k_pack_d32<<<grid_for(n * cs), 256, 0, ctx->stream>>>(D, ldd, n, ncols, 0, cs, D32);
+        const bool acc64 = ctx->matmul_acc64;
+        void *Dm = ctx->ws.get("mm_Dm", (size_t)n * cs * (acc64 ? 8 : 4));
+        if (acc64)
+            k_pack_dm<double><<<grid_for(n * cs), 256, 0, ctx->stream>>>(D, ldd, n, ncols, cs,
+                                                                         (double *)Dm);
+        else
+            k_pack_dm<float><<<grid_for(n * cs), 256, 0, ctx->stream>>>(D, ldd, n, ncols, cs,
+                                                                        (float *)Dm);
         BBMM_LAUNCH_CHECK();
         ctx->launches++;
         if (nloc == 0) return;
@@ -316,10 +329,11 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
             const int64_t ldk = ((n + 3) / 4) * 4;
             float *Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
             build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
-            splits = kernel_matmul_stored(ctx, Kst, n, nloc, D32, cp, Vpart, cap, nullptr, nullptr);
+            splits = kernel_matmul_stored(ctx, Kst, n, nloc, Dm, acc64, cp, Vpart, cap, nullptr,
+                                          nullptr);
         } else {
-            splits = kernel_matmul_onthefly(ctx, h.kind, Xs, dp, n, rr.r0, nloc, D32, cp, h.s, Vpart,
-                                            cap, nullptr, nullptr);
+            splits = kernel_matmul_onthefly(ctx, h.kind, Xs, dp, n, rr.r0, nloc, Dm, acc64, cp,
+                                            h.s, Vpart, cap, nullptr, nullptr);
         }
         k_matmul_finish<<<grid_for(nloc * ncols), 256, 0, ctx->stream>>>(
             Vpart, splits, cs, nloc, ncols, h.noise_var, D, ldd, rr.r0, V, ldv);

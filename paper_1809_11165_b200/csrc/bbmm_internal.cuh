@@ -97,6 +97,7 @@ struct bbmm_ctx_s {
     std::string err;
     bbmm::Workspace ws;
     int launches = 0;   // library kernel launches since last reset
+    bool matmul_acc64 = true;   // BBMM_MATMUL_FP64ACC (default) / FP32ACC
 };
 
 namespace bbmm {
@@ -121,13 +122,15 @@ void scale_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper
 
 // Kernel-matmul: Vpart[s][i][cp] (fp64) = sum_{j in split s} k(x_{r0+i}, x_j) D32[j][.]
 // (outputscale applied, no sigma^2 term).  Returns number of splits used.
+// Dm: the search directions as the matmul reads them: n_pad x round4(cp),
+// fp64 when acc64 (default precision) else fp32.
 int kernel_matmul_onthefly(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n,
-                           int64_t r0, int64_t nloc, const float *D32, int cp, double s,
+                           int64_t r0, int64_t nloc, const void *Dm, bool acc64, int cp, double s,
                            double *Vpart, size_t vpart_cap_elems, cudaEvent_t ev0,
                            cudaEvent_t ev1);
 int kernel_matmul_stored(bbmm_ctx_s *ctx, const float *Kst, int64_t n, int64_t nloc,
-                         const float *D32, int cp, double *Vpart, size_t vpart_cap_elems,
-                         cudaEvent_t ev0, cudaEvent_t ev1);
+                         const void *Dm, bool acc64, int cp, double *Vpart,
+                         size_t vpart_cap_elems, cudaEvent_t ev0, cudaEvent_t ev1);
 void build_stored_k(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
                     int64_t nloc, double s, float *Kst);
 size_t vpart_elems(int64_t n, int64_t nloc, int cp, bool stored);

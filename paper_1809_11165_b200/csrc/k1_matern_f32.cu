@@ -1,0 +1,9 @@
+// k1_matern_f32.cu -- instantiations of K1 (Matern-5/2, fp32-chunked accumulation).
+#include "k1_kernels.cuh"
+
+namespace bbmm {
+void launch_k1_matern_f32(bbmm_ctx_s *ctx, int dp, int cp, const float *Xs, int64_t n, int64_t r0,
+                      int64_t nloc, const void *Dm, double s, double *Vpart, int splits) {
+    launch_k1_variant<1, false>(ctx, dp, cp, Xs, n, r0, nloc, Dm, s, Vpart, splits);
+}
+}  // namespace bbmm

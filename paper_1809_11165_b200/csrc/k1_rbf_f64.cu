@@ -1,0 +1,9 @@
+// k1_rbf_f64.cu -- instantiations of K1 (RBF, fp64 accumulation).
+#include "k1_kernels.cuh"
+
+namespace bbmm {
+void launch_k1_rbf_f64(bbmm_ctx_s *ctx, int dp, int cp, const float *Xs, int64_t n, int64_t r0,
+                      int64_t nloc, const void *Dm, double s, double *Vpart, int splits) {
+    launch_k1_variant<0, true>(ctx, dp, cp, Xs, n, r0, nloc, Dm, s, Vpart, splits);
+}
+}  // namespace bbmm

@@ -6,7 +6,7 @@
 //
 // Data layout (local rows of this rank, row-major, fp64):
 //   U, R, Z, D, V : nloc x c        (ld = c)
-//   D32           : n_pad x CS fp32 (all rows; this rank writes rows r0..r1;
+//   Dm            : n_pad x CS fp64/fp32 matmul copy of D (all rows; this rank writes r0..r1;
 //                                    the all-gather fills the rest)
 //   L             : k x n fp64      (row m = pivoted-Cholesky column m)
 // One iteration j (textbook signs, reading R5/R6):
@@ -281,10 +281,12 @@ __global__ void k_beta(MbcgState *st, const double *__restrict__ rz, double *__r
     if (col == 0) st->any_active = any;
 }
 
-// Pass D: D = Z + beta D (active), 0 (frozen); D32 rows r0.. (fp32, stride cs);
-// block 0 advances the iteration counter.
+// Pass D: D = Z + beta D (active), 0 (frozen); the matmul copy Dm of the local
+// rows (fp64 or fp32, stride cs, at global row positions r0..); block 0
+// advances the iteration counter.
+template <typename DT>
 __global__ void k_passD(MbcgState *st, const double *__restrict__ Z, int64_t nloc, int c,
-                        int64_t r0, int cs, double *__restrict__ D, float *__restrict__ D32,
+                        int64_t r0, int cs, double *__restrict__ D, DT *__restrict__ Dm,
                         int advance) {
     const int col = threadIdx.x;
     if (col < cs) {
@@ -295,12 +297,11 @@ __global__ void k_passD(MbcgState *st, const double *__restrict__ Z, int64_t nlo
             double dn = 0.0;
             if (act) dn = Z[i * c + col] + b * D[i * c + col];
             if (col < c) D[i * c + col] = dn;
-            D32[(r0 + i) * cs + col] = (float)dn;
+            Dm[(r0 + i) * cs + col] = (DT)dn;
         }
     }
     if (advance && blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
-        // every thread of every block has read st->beta/active before any
-        // kernel that follows in stream order; j is only read by later kernels
+        // j is only read by kernels that follow in stream order
         st->j += 1;
     }
 }
@@ -467,7 +468,9 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     double *D = (double *)ws.get("cg_D", nc * 8);
     double *V = (double *)ws.get("cg_V", nc * 8);
     const int64_t npad = a.nb * ctx->nranks;
-    float *D32 = (float *)ws.get("cg_D32", (size_t)npad * cs * 4);
+    const bool acc64 = ctx->matmul_acc64;
+    const size_t esz = acc64 ? 8 : 4;
+    void *Dm = ws.get("cg_Dm", (size_t)npad * cs * esz);
     size_t vcap = vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
     double *Vpart = (double *)ws.get("cg_Vpart", std::max<size_t>(vcap, 1) * 8);
     const PassGeom g = pass_geom(nloc, c);
@@ -481,7 +484,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     double *bhist = (double *)ws.get("cg_bhist", (size_t)a.max_iter * c * 8);
     BBMM_CUDA(cudaMemsetAsync(ahist, 0, (size_t)a.max_iter * c * 8, sm));
     BBMM_CUDA(cudaMemsetAsync(bhist, 0, (size_t)a.max_iter * c * 8, sm));
-    BBMM_CUDA(cudaMemsetAsync(D32, 0, (size_t)npad * cs * 4, sm));
+    BBMM_CUDA(cudaMemsetAsync(Dm, 0, (size_t)npad * cs * esz, sm));
     const size_t smem_S = (size_t)kk * c * 8;
     if (smem_S > 48 * 1024)
         BBMM_CUDA(cudaFuncSetAttribute(k_precond_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -523,9 +526,18 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         k_copy<<<256, 256, 0, sm>>>(Z, out.Z0, (int64_t)nc);
         launches++;
     }
-    k_passD<<<g.grid, dim3(cs <= 32 ? 32 : 64, g.rb), 0, sm>>>(st, Z, nloc, c, a.r0, cs, D, D32, 0);
-    launches++;
-    if (multi) allgather_rows(ctx, D32, (size_t)a.nb * cs * 4);
+    auto passD = [&](int advance) {
+        dim3 blk(cs <= 32 ? 32 : 64, g.rb);
+        if (acc64)
+            k_passD<double><<<g.grid, blk, 0, sm>>>(st, Z, nloc, c, a.r0, cs, D, (double *)Dm,
+                                                    advance);
+        else
+            k_passD<float><<<g.grid, blk, 0, sm>>>(st, Z, nloc, c, a.r0, cs, D, (float *)Dm,
+                                                   advance);
+        launches++;
+        if (multi) allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
+    };
+    passD(0);
     BBMM_LAUNCH_CHECK();
 
     // ---------------- iterations
@@ -544,10 +556,11 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         mm_ev.push_back(e1);
         int splits;
         if (a.Kst)
-            splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, D32, cp, Vpart, vcap, e0, e1);
+            splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, Dm, acc64, cp, Vpart, vcap, e0,
+                                          e1);
         else
-            splits = kernel_matmul_onthefly(ctx, a.kind, a.Xs, a.dp, a.n, a.r0, nloc, D32, cp, a.s,
-                                            Vpart, vcap, e0, e1);
+            splits = kernel_matmul_onthefly(ctx, a.kind, a.Xs, a.dp, a.n, a.r0, nloc, Dm, acc64,
+                                            cp, a.s, Vpart, vcap, e0, e1);
         k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
         reduce(c, red);
         if (multi) allreduce_sum(ctx, red, c);
@@ -562,10 +575,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         reduce(c, red_rz);
         if (multi) allreduce_sum(ctx, red_rz, c);
         k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
-        k_passD<<<g.grid, dim3(cs <= 32 ? 32 : 64, g.rb), 0, sm>>>(st, Z, nloc, c, a.r0, cs, D,
-                                                                    D32, 1);
-        launches += 8;
-        if (multi) allgather_rows(ctx, D32, (size_t)a.nb * cs * 4);
+        launches += 7;
+        passD(1);
         BBMM_LAUNCH_CHECK();
         iters_run = j + 1;
         if (a.tol > 0.0) {
