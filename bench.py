@@ -142,7 +142,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kmode", default=None, choices=[None, "onthefly", "stored"])
-    ap.add_argument("--precision", default="fp64acc", choices=["fp64acc", "fp32acc"])
+    ap.add_argument("--precision", default="int8exact", choices=["int8exact", "fp64acc", "fp32acc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -167,7 +167,8 @@ def main():
     kmode = {"onthefly": bb.ONTHEFLY, "stored": bb.STORED}.get(
         args.kmode, bb.STORED if cfg.stored else bb.ONTHEFLY)
     ctx = bb.Context(local_rank)
-    ctx.set_matmul_precision(bb.FP64ACC if args.precision == "fp64acc" else bb.FP32ACC)
+    ctx.set_matmul_precision({"int8exact": bb.INT8EXACT, "fp64acc": bb.FP64ACC,
+                              "fp32acc": bb.FP32ACC}[args.precision])
     if world > 1:
         ctx.set_comm()
     X = torch.from_numpy(pr.X).cuda()
@@ -257,7 +258,10 @@ def main():
     tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    roofline = {"bound": "alu", "kernel": "k1_onthefly (Khat*D)", "achieved": achieved,
+    path = stats[-1]["matmul_path"]
+    kname = {0: "k1_onthefly (CUDA-core Khat*D)", 1: "k2_stored (Khat*D)",
+             2: "k1tc2_rbf (tcgen05 exact Khat*D)"}[path]
+    roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
                 "peak": peak_exp, "unit": "Gop/s (MUFU ex2/sqrt)", "frac": achieved / peak_exp,
                 "traffic": traffic,
                 "peak_source": f"derived: 16 MUFU ops/clk/SM x 148 SMs x {f_mhz:.0f} MHz "
@@ -282,7 +286,8 @@ def main():
         "roofline": roofline, "e2e": e2e, "gpu_launches": launches // max(len(stats), 1) * args.steps,
         "clocks": clocks,
         "detail": {k: stats[-1][k] for k in ("ms_pivchol", "ms_mbcg", "ms_matmul", "ms_slq",
-                                               "ms_deriv", "iters", "k_used", "logdet")},
+                                               "ms_deriv", "iters", "k_used", "logdet",
+                                               "matmul_path")},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, pr)

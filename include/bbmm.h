@@ -68,14 +68,24 @@ typedef enum { BBMM_RBF = 0, BBMM_MATERN52 = 1 } bbmm_kernel_t;
 typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
 
 /* Arithmetic of the blackbox matmul Khat*D.
- * FP64ACC (default): kernel values in fp32 (MUFU ex2/sqrt), search directions
+ * FP64ACC: kernel values in fp32 (MUFU ex2/sqrt), search directions
  *   D in fp64, products and sums in fp64.  Parity with the fp64 oracle holds
  *   whether or not mBCG has converged by max_iter (a per-iteration fp32
  *   rounding of D is amplified by an unconverged Krylov process).
  * FP32ACC: D rounded to fp32, products summed in fp32 over 16 terms then
  *   folded into fp64.  Faster; parity holds only where mBCG has converged
  *   (SURVEY.md §8c "regime A"). */
-typedef enum { BBMM_MATMUL_FP64ACC = 0, BBMM_MATMUL_FP32ACC = 1 } bbmm_matmul_precision_t;
+/* INT8EXACT (default): tcgen05 tensor cores; kernel values as 22-bit fixed
+ *   point, D as 31-bit fixed point (per-column scale), products and sums EXACT
+ *   in int32 (drained to fp64); the exponent comes from a 3xTF32 tensor-core
+ *   distance.  Used for on-the-fly RBF when the shape is supported (d <= 22,
+ *   t + 1 in {1,2,4,8,11}; d <= 6 for t + 1 = 17) and
+ *   max |x_scaled|^2 <= 16 (precision guard); otherwise FP64ACC is used. */
+typedef enum {
+    BBMM_MATMUL_FP64ACC = 0,
+    BBMM_MATMUL_FP32ACC = 1,
+    BBMM_MATMUL_INT8EXACT = 2
+} bbmm_matmul_precision_t;
 
 typedef struct {
     int32_t kind;            /* bbmm_kernel_t */
@@ -103,6 +113,9 @@ typedef struct {
     double ms_deriv;         /* derivative pass */
     int32_t matmul_launches; /* K-hat*D kernel launches inside ms_matmul */
     int32_t gpu_launches;    /* library kernels launched by the call */
+    int32_t matmul_path;     /* 0 on-the-fly CUDA-core (FP64ACC/FP32ACC),
+                                1 stored K, 2 tcgen05 exact (INT8EXACT) */
+    int32_t reserved_;
 } bbmm_stats_t;
 
 /* ---- context ----------------------------------------------------------- */
@@ -122,7 +135,7 @@ const char *bbmm_version(void);
 bbmm_status_t bbmm_nccl_unique_id(void *out_128_bytes);
 bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank,
                                 const void *nccl_unique_id_128_bytes);
-/* Select the matmul arithmetic for subsequent calls on ctx (default FP64ACC). */
+/* Select the matmul arithmetic for subsequent calls on ctx (default INT8EXACT). */
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p);
 /* Local row range [*r0, *r1) of this rank for problem size n. */
 bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0,

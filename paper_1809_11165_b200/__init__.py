@@ -24,8 +24,9 @@ RBF = 0
 MATERN52 = 1
 ONTHEFLY = 0
 STORED = 1
-FP64ACC = 0     # matmul precision (default): fp64 D, fp64 products and sums
+FP64ACC = 0     # matmul precision: fp64 D, fp64 products and sums (FFMA/DFMA path)
 FP32ACC = 1     # fp32 D, 16-term fp32 chunks folded into fp64 (regime A only)
+INT8EXACT = 2   # default: tcgen05 int8 tensor cores, exact integer contraction (RBF; else FP64ACC)
 
 _STATUS = {0: "OK", 2: "ERR_ARG", 3: "ERR_DATA", 4: "ERR_NUMERIC", 5: "ERR_CUDA",
            6: "ERR_NCCL", 7: "ERR_OOM"}
@@ -55,7 +56,8 @@ class Stats(C.Structure):
                 ("resid_trace", C.c_double), ("relres_y", C.c_double), ("ms_total", C.c_double),
                 ("ms_pivchol", C.c_double), ("ms_mbcg", C.c_double), ("ms_matmul", C.c_double),
                 ("ms_slq", C.c_double), ("ms_deriv", C.c_double),
-                ("matmul_launches", C.c_int32), ("gpu_launches", C.c_int32)]
+                ("matmul_launches", C.c_int32), ("gpu_launches", C.c_int32),
+                ("matmul_path", C.c_int32), ("reserved_", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

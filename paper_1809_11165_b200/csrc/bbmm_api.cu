@@ -37,7 +37,9 @@ void Workspace::release_all() {
 
 RowRange local_rows(const bbmm_ctx_s *ctx, int64_t n) {
     RowRange r;
-    r.nb = ceil_div(n, ctx->nranks);
+    // row blocks are multiples of 128 so rank boundaries align with the
+    // j-tiles of the tensor-core operand (k1tc) and the all-gathers.
+    r.nb = ceil_div(ceil_div(n, ctx->nranks), 128) * 128;
     r.r0 = std::min<int64_t>(n, (int64_t)ctx->rank * r.nb);
     r.r1 = std::min<int64_t>(n, r.r0 + r.nb);
     return r;
@@ -67,6 +69,11 @@ Hyper make_hyper(const bbmm_hyper_t *hp, int d) {
 void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count) {
     if (ctx->nranks <= 1) return;
     BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count) {
+    if (ctx->nranks <= 1) return;
+    BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream));
 }
 
 void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank) {
@@ -282,8 +289,11 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
 }
 
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p) {
-    if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC)) return BBMM_ERR_ARG;
-    ctx->matmul_acc64 = (p == BBMM_MATMUL_FP64ACC);
+    if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC &&
+                 p != BBMM_MATMUL_INT8EXACT))
+        return BBMM_ERR_ARG;
+    ctx->matmul_acc64 = (p != BBMM_MATMUL_FP32ACC);
+    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT);
     return BBMM_OK;
 }
 
@@ -322,6 +332,24 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
         ctx->launches++;
         if (nloc == 0) return;
         const bool stored = kmode == BBMM_STORED;
+        TcOperand op = stored ? TcOperand{} : tc_prepare(ctx, X, n, d, ncols, h, n);
+        if (op.version != 0) {
+            const int64_t npad = k1tc_pad_rows(n);
+            double *S = (double *)ctx->ws.get("tc_S", kMaxCols * 8);
+            k1tc_colmax(ctx, D, ldd, n, ncols, S);
+            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * k1tc_bslice_rows(ncols));
+            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp);
+            size_t cap = tc_vpart_elems(op, n, nloc, ncols);
+            double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
+            int splits = tc_matmul(ctx, op, Bp, S, ncols, n, rr.r0, nloc, h.s, Vpart, cap, nullptr,
+                                   nullptr);
+            k_matmul_finish<<<grid_for(nloc * ncols), 256, 0, ctx->stream>>>(
+                Vpart, splits, (ncols + 3) & ~3, nloc, ncols, h.noise_var, D, ldd, rr.r0, V, ldv);
+            BBMM_LAUNCH_CHECK();
+            ctx->launches++;
+            BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
         size_t cap = vpart_elems(n, nloc, cp, stored);
         double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
         int splits;
@@ -390,7 +418,8 @@ bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
             Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
             build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
         }
-        MbcgArgs a{Xs, dp, h.kind, h.s, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L, k, ncols,
+        TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, ncols, h, rr.nb * ctx->nranks);
+        MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L, k, ncols,
                    max_iter, tol};
         MbcgOut o;
         o.U = U;
@@ -460,7 +489,8 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         }
 
         // 3. one mBCG call on [y, z_1..z_t]
-        MbcgArgs a{Xs, dp, h.kind, h.s, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
+        TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, c, h, rr.nb * ctx->nranks);
+        MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
                    k > 0 ? k_used : 0, c, max_iter, tol};
         MbcgOut o;
         o.Z0 = Z0;
@@ -552,6 +582,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             s.ms_deriv = t_end.since(t_slq);
             s.matmul_launches = o.matmul_launches;
             s.gpu_launches = ctx->launches - launches0;
+            s.matmul_path = tcop.version == 2 ? 2 : (Kst ? 1 : 0);
             *stats_h = s;
         }
         BBMM_CUDA(cudaStreamSynchronize(sm));

@@ -97,7 +97,8 @@ struct bbmm_ctx_s {
     std::string err;
     bbmm::Workspace ws;
     int launches = 0;   // library kernel launches since last reset
-    bool matmul_acc64 = true;   // BBMM_MATMUL_FP64ACC (default) / FP32ACC
+    bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
+    bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
 };
 
 namespace bbmm {
@@ -135,6 +136,39 @@ void build_stored_k(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t 
                     int64_t nloc, double s, float *Kst);
 size_t vpart_elems(int64_t n, int64_t nloc, int cp, bool stored);
 
+// ------------------------------------------- tensor-core matmul (k1tc.cu)
+int64_t k1tc_pad_rows(int64_t n);
+int k1tc_bslice_rows(int c);
+void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean);
+void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, int c, double *S);
+void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
+               int64_t n, int c, const double *S, uint8_t *Bpack);
+void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count);
+bool k1tc2_supported(int kind, int d, int c);
+int64_t k1tc2_xa_floats(int64_t npad, int d);
+int64_t k1tc2_xb_floats(int64_t npad, int d);
+float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h,
+                        float *Xa, float *XB, int64_t npad);
+size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c);
+int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
+                 const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1);
+
+// Tensor-core operand of one mBCG call (prepared once per call).
+struct TcOperand {
+    int version = 0;            // 0: none (FP64ACC path), 2: k1tc2
+    int d = 0;
+    const float *Xa = nullptr;  // v2 row operand
+    const float *XB = nullptr;  // v2 distance tiles
+};
+// Prepare the tensor-core inputs for (kind, d, c) if the INT8EXACT mode applies.
+TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, const Hyper &h,
+                     int64_t npad_rows);
+size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c);
+int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
+              int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
+              cudaEvent_t ev0, cudaEvent_t ev1);
+
 // ------------------------------------------------------- pivchol.cu
 void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, int k,
              double *L, int64_t *piv_h, int *k_used_h, double *resid_h);
@@ -142,6 +176,7 @@ void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, 
 // ----------------------------------------------------------- mbcg.cu
 struct MbcgArgs {
     const float *Xs; int dp; int kind; double s;   // on-the-fly operator
+    TcOperand tc;                                   // tensor-core operand (version 0: none)
     const float *Kst;                               // stored operator (or null)
     int64_t n; int64_t r0; int64_t nloc; int64_t nb;
     double noise_var;

@@ -1,0 +1,151 @@
+// k1tc.cu -- operand preparation shared by the tensor-core kernel-matmul
+// (k1tc2.cu): per-column scales of the search directions and their packing
+// into the int8 slice tiles the tcgen05 MMAs consume, plus the input mean.
+//
+// Packed operand:
+//   D_jc  -> P'_jc = round(D_jc / S_c 2^30) + 2^30 in [0, 2^31], four u8
+//            slices p3 p2 p1 p0 (S_c = max_j |D_jc|); one extra constant
+//            column with P' = 2^30 removes the offset exactly.
+#include <algorithm>
+#include <cmath>
+
+#include "bbmm_internal.cuh"
+#include "pair_common.cuh"
+
+namespace bbmm {
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int STAGES = 3;
+constexpr int WINDOW = 16384;                 // j per TMEM drain (int32 bound)
+constexpr int kThreads = 192;
+constexpr __host__ __device__ int round16(int x) { return (x + 15) & ~15; }
+constexpr __host__ __device__ int round32(int x) { return (x + 31) & ~31; }
+
+__global__ void k_col_mean(const float *__restrict__ X, int64_t n, int d, double *__restrict__ mean) {
+    const int q = blockIdx.x;
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) s += (double)X[j * d + q];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) mean[q] = sh[0] / (double)n;
+}
+
+// per-block partial max |D_c| over rows (threadIdx.x = column)
+__global__ void k_colmax_part(const double *__restrict__ D, int64_t ldd, int64_t rows, int c,
+                              double *__restrict__ part) {
+    const int col = threadIdx.x;
+    __shared__ double sh[256];
+    double m = 0.0;
+    if (col < c)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < rows;
+             i += (int64_t)gridDim.x * blockDim.y)
+            m = fmax(m, fabs(D[i * ldd + col]));
+    sh[threadIdx.y * blockDim.x + col] = m;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < c) {
+        for (int y = 1; y < blockDim.y; y++) m = fmax(m, sh[y * blockDim.x + col]);
+        part[(int64_t)blockIdx.x * c + col] = m;
+    }
+}
+__global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c, double *__restrict__ S) {
+    const int col = threadIdx.x;
+    if (col >= c) return;
+    double m = 0.0;
+    for (int b = 0; b < nblk; b++) m = fmax(m, part[(int64_t)b * c + col]);
+    S[col] = m > 0.0 ? m : 1.0;
+}
+
+// Pack rows [row0, row0 + rows) of D (fp64) into the per-tile K-major slice
+// layout: tile tt = j / BK holds NB rows (n = b_idx * C1 + col; b_idx 0..3 =
+// bytes 3..0 of P' = round(D/S 2^30) + 2^30; col == C is the constant 2^30)
+// of BK bytes, as [BK/16 chunks][NB rows][16 bytes].  One thread writes the
+// 16 bytes of one (tile, chunk, n).
+__global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_t row0,
+                               int64_t rows, int64_t n, int c, int C1, int NB,
+                               const double *__restrict__ S, uint8_t *__restrict__ Bpack,
+                               int64_t tile0, int64_t tiles) {
+    const int64_t total = tiles * (BK / 16) * NB;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int nn = (int)(e % NB);
+        const int64_t rest = e / NB;
+        const int kc = (int)(rest % (BK / 16));
+        const int64_t tt = tile0 + rest / (BK / 16);
+        const int bi = nn / C1, col = nn - bi * C1;
+        uint32_t wv[4] = {0, 0, 0, 0};
+        if (bi < 4) {
+            const int shift = 8 * (3 - bi);
+#pragma unroll
+            for (int p = 0; p < 16; p++) {
+                const int64_t j = tt * BK + kc * 16 + p;       // global point index
+                uint32_t byte = 0;
+                if (j < n && j >= row0 && j < row0 + rows) {
+                    int64_t P;
+                    if (col < c) {
+                        double q = D[(j - row0) * ldd + col] / S[col] * 1073741824.0;
+                        P = llrint(q) + 1073741824LL;          // in [0, 2^31]
+                    } else {
+                        P = 1073741824LL;                      // constant column
+                    }
+                    byte = (uint32_t)((P >> shift) & 0xFF);
+                }
+                wv[p >> 2] |= byte << (8 * (p & 3));
+            }
+        }
+        uint8_t *dst = Bpack + tt * (int64_t)NB * BK + (int64_t)kc * NB * 16 + (int64_t)nn * 16;
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+}
+
+}  // namespace tc
+
+// ======================================================================
+// host side
+// ======================================================================
+int k1tc_bslice_rows(int c) { return tc::round16(4 * (c + 1)); }
+
+void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean) {
+    tc::k_col_mean<<<d, 256, 0, ctx->stream>>>(X, n, d, mean);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+int64_t k1tc_pad_rows(int64_t n) { return ceil_div(n, 128) * 128; }   // covers both tile widths
+
+// S (c doubles, device): column max |D| over the rows given (local rows);
+// caller all-reduces (max) across ranks if needed.
+void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, int c, double *S) {
+    const int cw = c <= 32 ? 32 : 64, rb = 256 / cw;
+    int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, rb), 2 * kNumSMs));
+    double *part = (double *)ctx->ws.get("tc_cmax", (size_t)nblk * c * 8);
+    tc::k_colmax_part<<<nblk, dim3(cw, rb), 0, ctx->stream>>>(D, ldd, rows, c, part);
+    tc::k_colmax_final<<<1, 64, 0, ctx->stream>>>(part, nblk, c, S);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches += 2;
+}
+
+// Pack local rows [row0, row0 + rows) into Bpack (tiles covering them).
+void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
+               int64_t n, int c, const double *S, uint8_t *Bpack) {
+    const int C1 = c + 1, NB = tc::round16(4 * C1);
+    // cover the rows up to the next multiple of 128 (the widest j-tile any
+    // consumer reads); rows >= n are written as zeros
+    const int64_t tile0 = row0 / tc::BK;
+    const int64_t tiles = ceil_div(ceil_div(row0 + rows, 128) * 128, tc::BK) - tile0;
+    const int64_t total = tiles * (tc::BK / 16) * NB;
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
+    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, C1, NB, S, Bpack,
+                                                      tile0, tiles);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+}  // namespace bbmm

@@ -1,0 +1,480 @@
+// k1tc2.cu -- Blackwell tensor-core kernel-matmul, version 2 (K1-TC2).
+//
+// Same exact int8 contraction as k1tc.cu (DESIGN.md "K1-TC exact
+// contraction"), but with both operand streams that limited version 1 (the
+// shared-memory pipe: x_j broadcasts, A-tile stores, A reads by the MMA)
+// moved into tensor memory:
+//   * the exponent S_ij = -|xs_i - xs_j|^2 is itself a tcgen05 MMA (kind::tf32,
+//     "3xTF32" split for fp32-level accuracy) of augmented vectors
+//       A_i = [2 xs_i, -|xs_i|^2, 1],  B_j = [xs_j, 1, -|xs_j|^2]
+//     with A resident in TMEM for the CTA's rows and B_j streamed per tile;
+//     S lands in TMEM and is read with one tcgen05.ld per 32 j;
+//   * the int8 slices of the quantised kernel values are written straight
+//     to TMEM (tcgen05.st) and consumed as the A operand of the int8 MMAs.
+// Per pair a compute thread then issues ~5 instructions (ex2, 1 FFMA,
+// byte permutes) so the kernel is bound by the MUFU ex2 pipe.
+//
+// CTA = 128 rows, 1 CTA per SM, 19 warps:
+//   warps 0-15: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
+//               h = w / 4 (16 of the 64 j) of every j tile
+//   warp 16   : producer (bulk copies of the B' distance tile and the packed
+//               D slices)
+//   warp 17   : MMA issuer for the int8 contraction of tile t
+//   warp 18   : MMA issuer for the distance MMAs (runs up to 2 tiles ahead)
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "bbmm_internal.cuh"
+#include "pair_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace bbmm {
+namespace tc2 {
+
+// j-tile BK = 128; 16 compute warps, warp (sub, h) serves TMEM lanes
+// 32 sub.. and the j-group h (32 j) of every tile.  Each TMEM stage buffer
+// (128 columns) first receives S (fp32, from the distance MMA); every warp
+// then overwrites ITS OWN 32 S columns with the three int8 slices of its
+// quantised kernel values (24 columns), which the int8 MMAs read as A.
+constexpr int BM = 128, BK = 128, STAGES = 3, NBUF = 2;
+constexpr int WINDOW = 16384;
+constexpr int NQ = 4, JW = BK / NQ, NCW = 4 * NQ;
+constexpr int kThreads = 32 * (NCW + 3);
+constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1, DIST_WARP = NCW + 2;
+static_assert(JW == 32, "one 32-column group per warp");
+constexpr __host__ __device__ int r16(int x) { return (x + 15) & ~15; }
+constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
+
+template <int C, int DA>
+struct Cfg {
+    static constexpr int C1 = C + 1;
+    static constexpr int NB = r16(4 * C1), NQ1 = r16(3 * C1), NQ0 = r16(2 * C1);
+    static constexpr int OFF1 = r32(NB), OFF0 = OFF1 + r32(NQ1);
+    static constexpr int ACC_END = OFF0 + r32(NQ0);
+    static constexpr int AP_OFF = ACC_END;                     // 3 DA tf32 columns
+    static constexpr int BUF_OFF = r32(AP_OFF + 3 * DA);       // NBUF x BK columns
+    static constexpr int END = BUF_OFF + NBUF * BK;
+    static_assert(END <= 512, "TMEM budget exceeded");
+    static constexpr int B8_BYTES = NB * BK;                   // int8 D slices per tile
+    static constexpr int XB_BYTES = 3 * DA * BK * 4;           // tf32 B' per tile
+    static constexpr int STAGE_BYTES = B8_BYTES + XB_BYTES;
+    // >= 120 KB so that a single CTA (which owns all 512 TMEM columns) is resident per SM
+    static constexpr int SMEM = (STAGES * STAGE_BYTES + 1024) > 122880 ? (STAGES * STAGE_BYTES + 1024) : 122880;
+};
+
+// Drain one window's int32 accumulators of this thread's row (TMEM lane)
+// into the fp64 sums acc_sm[c][rl] (c == C: constant offset column).
+// Region a (2, 1, 0 = slices q2 q1 q0) holds column blocks bi = 0..3 of the D
+// slices p3 p2 p1 p0 (weight 2^(8a + 8(3 - bi))), bmax = 4, 3, 2 blocks kept.
+template <int C, int C1>
+__device__ __noinline__ void drain_window(uint32_t lane_base, int nb, int off1, int nq1, int off0,
+                                          int nq0, double (*acc_sm)[BM], int rl) {
+    const int offs[3] = {0, off1, off0}, ns[3] = {nb, nq1, nq0};
+#pragma unroll 1
+    for (int reg = 0; reg < 3; reg++) {
+        const int a = 2 - reg, bmax = 4 - reg;
+#pragma unroll 1
+        for (int cb = 0; cb < ns[reg]; cb += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld32(lane_base + offs[reg] + cb, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int g = 0; g < 32; g++) {
+                const int col = cb + g;
+                const int bi = col / C1, cc = col - bi * C1;
+                if (bi < bmax) {
+                    const double w = ldexp(1.0, 8 * a + 8 * (3 - bi));
+                    acc_sm[cc][rl] = fma(w, (double)(int32_t)r[g], acc_sm[cc][rl]);
+                }
+            }
+        }
+    }
+}
+
+template <int C, int DA>
+__global__ void __launch_bounds__(kThreads, 1)
+k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
+          const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
+          int64_t nloc, int64_t tiles_per_split, int64_t ntiles, double s,
+          double *__restrict__ Vpart) {
+    using K = Cfg<C, DA>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full_b[STAGES], free_b[STAGES];
+    __shared__ __align__(8) uint64_t s_full[NBUF], a_full[NBUF], buf_free[NBUF];
+    __shared__ __align__(8) uint64_t acc_full, acc_empty, init_done;
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ double acc_sm[C + 1][BM];   // fp64 accumulators (+ constant column)
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
+    const int ntl = (int)(min(ntiles, t0 + tiles_per_split) - t0);
+    constexpr int TPW = WINDOW / BK;
+
+    if (tid == 0) {
+        for (int q = 0; q < STAGES; q++) {
+            ptx::mbar_init(&full_b[q], 1);
+            ptx::mbar_init(&free_b[q], 1);
+        }
+        for (int q = 0; q < NBUF; q++) {
+            ptx::mbar_init(&s_full[q], 1);
+            ptx::mbar_init(&a_full[q], 32 * NCW);
+            ptx::mbar_init(&buf_free[q], 1);
+        }
+        ptx::mbar_init(&acc_full, 1);
+        ptx::mbar_init(&acc_empty, 128);
+        ptx::mbar_init(&init_done, 128);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<512>(&tmem_base_sh);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == PRODUCER_WARP) {
+        // ------------------------------------------------------- producer
+        const bool leader = ptx::elect_one();
+        for (int t = 0; t < ntl; t++) {
+            const int st = t % STAGES;
+            const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+            if (leader) {
+                ptx::mbar_wait(&free_b[st], ph ^ 1);
+                uint8_t *sb = smem + st * K::STAGE_BYTES;
+                const int64_t tg = t0 + t;
+                ptx::mbar_arrive_expect_tx(&full_b[st], K::STAGE_BYTES);
+                ptx::bulk_g2s(sb, Bpack + tg * K::B8_BYTES, K::B8_BYTES, &full_b[st]);
+                ptx::bulk_g2s(sb + K::B8_BYTES, reinterpret_cast<const uint8_t *>(XB) + tg * K::XB_BYTES,
+                              K::XB_BYTES, &full_b[st]);
+            }
+            __syncwarp();
+        }
+    } else if (warp == DIST_WARP) {
+        // ----------------------------------- MMA issuer: distance S = A'.B'
+        constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
+        const bool leader = ptx::elect_one();
+        ptx::mbar_wait(&init_done, 0);
+        for (int t = 0; t < ntl; t++) {
+            const int st = t % STAGES;
+            const int b = t % NBUF;
+            ptx::mbar_wait(&full_b[st], (uint32_t)((t / STAGES) & 1));
+            ptx::mbar_wait(&buf_free[b], (uint32_t)(((t / NBUF) & 1) ^ 1));
+            ptx::tc_fence_after();
+            if (leader) {
+                const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
+#pragma unroll
+                for (int ks = 0; ks < 3 * DA / 8; ks++) {
+                    const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
+                    ptx::mma_tf32_ts(tmem + K::BUF_OFF + b * BK, tmem + K::AP_OFF + ks * 8, bd, IDS,
+                                     ks > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&s_full[b]);
+            }
+            __syncwarp();
+        }
+    } else if (warp == MMA_WARP) {
+        // ---------------------------- MMA issuer: exact int8 contraction
+        constexpr uint32_t ID2 = ptx::idesc_i8(BM, K::NB, false, false);
+        constexpr uint32_t ID1 = ptx::idesc_i8(BM, K::NQ1, false, false);
+        constexpr uint32_t ID0 = ptx::idesc_i8(BM, K::NQ0, false, false);
+        const bool leader = ptx::elect_one();
+        for (int t = 0; t < ntl; t++) {
+            const int st = t % STAGES;
+            const int b = t % NBUF;
+            const int win = t / TPW;
+            const bool first = (t % TPW) == 0;
+            if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
+            ptx::mbar_wait(&a_full[b], (uint32_t)((t / NBUF) & 1));
+            ptx::tc_fence_after();
+            if (leader) {
+                const uint32_t b8 = ptx::smem_u32(smem + st * K::STAGE_BYTES);
+                const uint32_t aq = tmem + K::BUF_OFF + b * BK;
+#pragma unroll
+                for (int ks = 0; ks < BK / 32; ks++) {
+                    const uint64_t bd = ptx::smem_desc_kmajor(b8 + ks * 2 * K::NB * 16, K::NB * 16, 128);
+                    const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                    ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, ID2, acc);       // q2
+                    ptx::mma_i8_ts(tmem + K::OFF1, aq + 32 * ks + 8, bd, ID1, acc);  // q1
+                    ptx::mma_i8_ts(tmem + K::OFF0, aq + 32 * ks + 0, bd, ID0, acc);  // q0
+                }
+                ptx::mma_commit(&buf_free[b]);
+                ptx::mma_commit(&free_b[st]);
+                if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
+            }
+            __syncwarp();
+        }
+    } else {
+        // -------------------------------------------------------- compute
+        const int sub = warp & 3, h = warp >> 2;
+        const int64_t row = (int64_t)blockIdx.x * BM + sub * 32 + lane;
+        const bool valid = row < nloc;
+        const uint32_t lane_base = tmem + ((uint32_t)(sub * 32) << 16);
+        if (h == 0) {
+            // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32)
+            uint32_t hi[DA], lo[DA];
+#pragma unroll
+            for (int q = 0; q < DA; q++) {
+                const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
+                const uint32_t vb = __float_as_uint(v) & 0xFFFFE000u;
+                hi[q] = vb;
+                lo[q] = __float_as_uint(v - __uint_as_float(vb));
+            }
+#pragma unroll
+            for (int q0 = 0; q0 < DA; q0 += 8) {
+                uint32_t a8[8], b8[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) { a8[u] = hi[q0 + u]; b8[u] = lo[q0 + u]; }
+                ptx::tmem_st8(lane_base + K::AP_OFF + q0, a8);
+                ptx::tmem_st8(lane_base + K::AP_OFF + DA + q0, a8);
+                ptx::tmem_st8(lane_base + K::AP_OFF + 2 * DA + q0, b8);
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&init_done);
+            for (int c = 0; c <= C; c++) acc_sm[c][sub * 32 + lane] = 0.0;
+        }
+        const uint32_t a_sfull = ptx::smem_u32(&s_full[0]);
+        const uint32_t a_afull = ptx::smem_u32(&a_full[0]);
+        const uint32_t a_accf = ptx::smem_u32(&acc_full), a_acce = ptx::smem_u32(&acc_empty);
+        const uint32_t my_col = lane_base + K::BUF_OFF + JW * h;
+        int win = 0;
+        for (int t = 0; t < ntl; t++) {
+            const int b = t % NBUF;
+            ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / NBUF) & 1));
+            ptx::tc_fence_after();
+            uint32_t sv[32];
+            const uint32_t col = my_col + b * BK;
+            ptx::tmem_ld32(col, sv);
+            ptx::tmem_ld_wait();
+            uint32_t w0[8], w1[8], w2[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                uint32_t q[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float kv = ex2_approx(__uint_as_float(sv[4 * u + v]));
+                    q[v] = __float_as_uint(fmaf(kv, 0.5f, 1.0f));
+                }
+                const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
+                const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
+                const uint32_t u01 = __byte_perm(q[0], q[1], 0x7351);
+                const uint32_t u23 = __byte_perm(q[2], q[3], 0x7351);
+                w0[u] = __byte_perm(t01, t23, 0x5410);
+                w2[u] = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
+                w1[u] = __byte_perm(u01, u23, 0x5410);
+            }
+            // overwrite this warp's own S columns with the A slices [q0 | q1 | q2]
+            ptx::tmem_st8(col + 0, w0);
+            ptx::tmem_st8(col + 8, w1);
+            ptx::tmem_st8(col + 16, w2);
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_a(a_afull + 8 * b);
+
+            const bool last_of_window = ((t + 1) % TPW) == 0 || t + 1 == ntl;
+            if (last_of_window && h == 0) {
+                ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
+                ptx::tc_fence_after();
+                drain_window<C, K::C1>(lane_base, K::NB, K::OFF1, K::NQ1, K::OFF0, K::NQ0, acc_sm,
+                                       sub * 32 + lane);
+                ptx::tc_fence_before();
+                ptx::mbar_arrive_a(a_acce);
+                win++;
+            }
+        }
+        if (h == 0 && valid) {
+            constexpr int CS = (C + 3) & ~3;
+            const int rl = sub * 32 + lane;
+            double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * CS;
+            const double base = s * 0x1p-52;
+            const double cacc = acc_sm[C][rl];
+#pragma unroll
+            for (int c = 0; c < C; c++) out[c] = base * Sc[c] * (acc_sm[c][rl] - cacc);
+#pragma unroll
+            for (int c = C; c < CS; c++) out[c] = 0.0;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+// ---------------------------------------------------------- operand prep
+// Per point: xs = (x - mean) scale (fp32), e = -|xs|^2.
+//   Xa[i]  = [2 xs_i (d), e_i, 1, 0..]            (DA floats, row operand)
+//   XB tile tt (BK points): B'_j = [xs_j, 1, e_j, 0..] split [hi | lo | hi]
+//   stored K-major for the MMA: [3 DA / 4 chunks][BK rows][4 floats].
+__global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad, int d, int DA,
+                           const float *__restrict__ scale, const double *__restrict__ mean,
+                           float *__restrict__ Xa, float *__restrict__ XB,
+                           unsigned int *__restrict__ max_sq_bits) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npad;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        float xs[kMaxDim];
+        float e = 0.0f;
+        for (int q = 0; q < d; q++) {
+            xs[q] = (j < n) ? (float)((double)X[j * d + q] - mean[q]) * scale[q] : 0.0f;
+            e = fmaf(xs[q], xs[q], e);
+        }
+        if (j < n) atomicMax(max_sq_bits, __float_as_uint(e));   // e >= 0: bits are ordered
+        e = -e;
+        const bool ok = j < n;
+        for (int q = 0; q < DA; q++) {
+            float a = 0.0f, b = 0.0f;
+            if (ok) {
+                if (q < d) { a = 2.0f * xs[q]; b = xs[q]; }
+                else if (q == d) { a = e; b = 1.0f; }
+                else if (q == d + 1) { a = 1.0f; b = e; }
+            }
+            Xa[j * DA + q] = a;
+            const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
+            const float bl = b - bh;
+            const int64_t tt = j / BK;
+            const int jj = (int)(j - tt * BK);
+            float *tile = XB + tt * (int64_t)(3 * DA * BK);
+            const float parts[3] = {bh, bl, bh};
+            for (int pt = 0; pt < 3; pt++) {
+                const int k = pt * DA + q;             // K index in [0, 3 DA)
+                tile[(k >> 2) * (BK * 4) + jj * 4 + (k & 3)] = parts[pt];
+            }
+        }
+    }
+}
+
+}  // namespace tc2
+
+// ======================================================================
+// host side
+// ======================================================================
+static int tc2_da(int d) { return ((d + 2 + 7) / 8) * 8; }
+
+bool k1tc2_supported(int kind, int d, int c) {
+    if (kind != BBMM_RBF) return false;
+    const int da = tc2_da(d);
+    switch (c) {
+        case 1: case 2: case 4: case 8: case 11: return da <= 24;
+        case 17: return da <= 8;
+        default: return false;
+    }
+}
+
+int64_t k1tc2_xa_floats(int64_t npad, int d) { return npad * tc2_da(d); }
+int64_t k1tc2_xb_floats(int64_t npad, int d) { return npad * 3 * tc2_da(d); }
+
+float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h,
+                        float *Xa, float *XB, int64_t npad) {
+    double *mean = (double *)ctx->ws.get("tc_mean", kMaxDim * 8);
+    float *sc_d = (float *)ctx->ws.get("tc_scale", kMaxDim * 4);
+    float sc[kMaxDim];
+    const double base = std::sqrt(0.5 / std::log(2.0));
+    for (int q = 0; q < d; q++) sc[q] = (float)(base / h.ls[h.n_ls == 1 ? 0 : q]);
+    BBMM_CUDA(cudaMemcpyAsync(sc_d, sc, sizeof(float) * d, cudaMemcpyHostToDevice, ctx->stream));
+    k1tc_col_mean(ctx, X, n, d, mean);
+    unsigned int *mx = (unsigned int *)ctx->ws.get("tc_maxsq", 4);
+    BBMM_CUDA(cudaMemsetAsync(mx, 0, 4, ctx->stream));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npad, 256), 4 * kNumSMs));
+    tc2::k_prep_tc2<<<grid, 256, 0, ctx->stream>>>(X, n, npad, d, tc2_da(d), sc_d, mean, Xa, XB,
+                                                   mx);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+    unsigned int mh = 0;
+    BBMM_CUDA(cudaMemcpyAsync(&mh, mx, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+    float mf;
+    std::memcpy(&mf, &mh, 4);
+    return mf;
+}
+
+template <int C, int DA>
+static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
+                      const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
+                      double *Vpart, size_t cap) {
+    using K = tc2::Cfg<C, DA>;
+    const int64_t ntiles = ceil_div(n, tc2::BK);
+    const int64_t rb = ceil_div(nloc, tc2::BM);
+    int64_t sp = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, rb), ntiles));
+    const int64_t tps = ceil_div(ntiles, sp);
+    sp = ceil_div(ntiles, tps);
+    BBMM_REQUIRE((size_t)sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k1tc2)");
+    static bool attr = false;
+    if (!attr) {
+        BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+        attr = true;
+    }
+    dim3 grid((unsigned)rb, (unsigned)sp);
+    tc2::k1tc2_rbf<C, DA><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(Xa, XB, Bp, S, r0, nloc,
+                                                                         tps, ntiles, s, Vpart);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+    return (int)sp;
+}
+
+size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c) {
+    const int64_t ntiles = ceil_div(n, tc2::BK);
+    const int64_t rb = ceil_div(std::max<int64_t>(nloc, 1), tc2::BM);
+    int64_t sp = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, rb), ntiles));
+    return (size_t)sp * std::max<int64_t>(nloc, 1) * ((c + 3) & ~3);
+}
+
+int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
+                 const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1) {
+    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    int sp = 1;
+    const int da = tc2_da(d);
+#define BBMM_TC2(CC, DD) \
+    if (c == CC && da == DD) sp = launch_tc2<CC, DD>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+    if (nloc > 0) {
+        BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
+        BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)
+        BBMM_TC2(11, 16) BBMM_TC2(1, 24) BBMM_TC2(2, 24) BBMM_TC2(4, 24)
+        BBMM_TC2(8, 24) BBMM_TC2(11, 24)
+        throw Error{BBMM_ERR_ARG, "k1tc2: unsupported (c, d)"};
+    }
+#undef BBMM_TC2
+    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    return sp;
+}
+
+// ------------------------------------------------ INT8EXACT dispatch
+TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, const Hyper &h,
+                     int64_t npad_rows) {
+    TcOperand op;
+    if (!ctx->matmul_tc) return op;
+    const int64_t npad = k1tc_pad_rows(npad_rows);
+    op.d = d;
+    if (k1tc2_supported(h.kind, d, c)) {
+        float *xa = (float *)ctx->ws.get("tc2_Xa", (size_t)k1tc2_xa_floats(npad, d) * 4);
+        float *xb = (float *)ctx->ws.get("tc2_XB", (size_t)k1tc2_xb_floats(npad, d) * 4);
+        const float max_sq = k1tc2_prep_inputs(ctx, X, n, d, h, xa, xb, npad);
+        // The expanded distance 2 xs_i.xs_j - |xs_i|^2 - |xs_j|^2 loses ~eps32 max|xs|^2
+        // absolutely; beyond max|xs|^2 = 16 (kernel-value error > ~1e-6) fall back to
+        // the direct-difference FP64ACC path.
+        if (!(max_sq <= 16.0f)) return op;
+        op.version = 2;
+        op.Xa = xa;
+        op.XB = xb;
+    }
+    return op;
+}
+
+size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c) {
+    (void)op;
+    return k1tc2_vpart_elems(n, nloc, c);
+}
+
+int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
+              int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
+              cudaEvent_t ev0, cudaEvent_t ev1) {
+    return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1);
+}
+
+}  // namespace bbmm

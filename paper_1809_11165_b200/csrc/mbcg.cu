@@ -471,7 +471,12 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     const bool acc64 = ctx->matmul_acc64;
     const size_t esz = acc64 ? 8 : 4;
     void *Dm = ws.get("cg_Dm", (size_t)npad * cs * esz);
-    size_t vcap = vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
+    const bool use_tc = a.tc.version != 0;
+    size_t vcap = use_tc ? tc_vpart_elems(a.tc, a.n, nloc, c) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
+    const int64_t npad_tc = use_tc ? k1tc_pad_rows(npad) : 0;
+    uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(c)) : nullptr;
+    double *Stc = use_tc ? (double *)ws.get("tc_S", kMaxCols * 8) : nullptr;
+    if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, (size_t)npad_tc * k1tc_bslice_rows(c), sm));
     double *Vpart = (double *)ws.get("cg_Vpart", std::max<size_t>(vcap, 1) * 8);
     const PassGeom g = pass_geom(nloc, c);
     const int nblk = (int)g.grid.x;
@@ -535,7 +540,15 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             k_passD<float><<<g.grid, blk, 0, sm>>>(st, Z, nloc, c, a.r0, cs, D, (float *)Dm,
                                                    advance);
         launches++;
-        if (multi) allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
+        if (use_tc) {
+            // tensor-core operand: global column scales, then int8 slices
+            k1tc_colmax(ctx, D, c, nloc, c, Stc);
+            if (multi) allreduce_max(ctx, Stc, c);
+            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp);
+            if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * k1tc_bslice_rows(c));
+        } else if (multi) {
+            allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
+        }
     };
     passD(0);
     BBMM_LAUNCH_CHECK();
@@ -555,7 +568,9 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         mm_ev.push_back(e0);
         mm_ev.push_back(e1);
         int splits;
-        if (a.Kst)
+        if (use_tc)
+            splits = tc_matmul(ctx, a.tc, Bp, Stc, c, a.n, a.r0, nloc, a.s, Vpart, vcap, e0, e1);
+        else if (a.Kst)
             splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, Dm, acc64, cp, Vpart, vcap, e0,
                                           e1);
         else

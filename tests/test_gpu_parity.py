@@ -46,17 +46,33 @@ MATMUL_CASES = [
 ]
 
 
+PRECISIONS = [bb.INT8EXACT, bb.FP64ACC, bb.FP32ACC]
+
+
+def matmul_bound(orc, pr, D):
+    """Per-element error bound of one Khat*D:
+    2e-6 relative to the absolute-value product (K|D| + sigma^2|D|, K >= 0),
+    plus the 22-bit fixed-point floor 2^-22 s sum_j |D_j| of the tensor-core
+    kernel values."""
+    absb = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D))
+    return 2e-6 * absb + 2.0**-22 * math.exp(pr.log_s) * np.abs(D).sum(0) + 1e-12
+
+
 @pytest.mark.parametrize("name,n,c", MATMUL_CASES)
 @pytest.mark.parametrize("kmode", [bb.ONTHEFLY, bb.STORED])
-def test_kernel_matmul_matches_oracle(ctx, orc, name, n, c, kmode):
+@pytest.mark.parametrize("prec", PRECISIONS)
+def test_kernel_matmul_matches_oracle(ctx, orc, name, n, c, kmode, prec):
     pr = synth.make_problem(synth.scaled(synth.CONFIGS[name], n), seed=3)
     D = synth.random_block(n, c, seed=4).astype(np.float64)
-    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), kmode).cpu().numpy()
+    ctx.set_matmul_precision(prec)
+    try:
+        V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), kmode).cpu().numpy()
+    finally:
+        ctx.set_matmul_precision(bb.INT8EXACT)
     ref = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
-    # summation bound: |err_i| <= tol * (K|D| + sigma^2 |D|)_i  (K >= 0)
-    absb = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D))
     err = np.abs(V - ref)
-    assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
+    bound = matmul_bound(orc, pr, D)
+    assert np.all(err <= bound), float((err / bound).max())
     assert colwise_rel(V, ref).max() < 2e-5
 
 
@@ -122,22 +138,28 @@ def test_mbcg_tolerance_freezes_columns(ctx, orc):
 MLL_CASES = [("C0", 256), ("C1", 3338), ("C2", 3000), ("C3", 2500), ("C4", 4000), ("C4", 1001)]
 
 
-def run_both(ctx, orc, cfg, seed=0, kmode=None, k=None, t=None):
+def run_both(ctx, orc, cfg, seed=0, kmode=None, k=None, t=None, prec=None):
     pr = synth.make_problem(cfg, seed=seed)
     k = cfg.k if k is None else k
     t = cfg.t if t is None else t
     km = (bb.STORED if cfg.stored else bb.ONTHEFLY) if kmode is None else kmode
-    g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), t, k, cfg.p, seed=7, kmode=km,
-                        return_solves=True)
+    if prec is not None:
+        ctx.set_matmul_precision(prec)
+    try:
+        g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), t, k, cfg.p, seed=7,
+                            kmode=km, return_solves=True)
+    finally:
+        ctx.set_matmul_precision(bb.INT8EXACT)
     o = orc.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, t, k, cfg.p,
                          seed=7)
     return pr, g, o
 
 
 @pytest.mark.parametrize("name,n", MLL_CASES)
-def test_mll_and_grad_matches_oracle(ctx, orc, name, n):
+@pytest.mark.parametrize("prec", [bb.INT8EXACT, bb.FP64ACC])
+def test_mll_and_grad_matches_oracle(ctx, orc, name, n, prec):
     cfg = synth.scaled(synth.CONFIGS[name], n)
-    pr, g, o = run_both(ctx, orc, cfg)
+    pr, g, o = run_both(ctx, orc, cfg, prec=prec)
     st = g["stats"]
     np.testing.assert_array_equal(g["pivots"], o["pivots"])
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
@@ -161,6 +183,20 @@ def test_edge_ranks_and_probe_counts(ctx, orc, k, t):
     pr, g, o = run_both(ctx, orc, cfg, k=k, t=t)
     assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
     assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
+
+
+def test_tensor_core_path_is_selected(ctx, orc):
+    """The default precision runs the tcgen05 kernel on the bench workload shape
+    (C4: RBF, d = 3, t + 1 = 17) and falls back where it does not apply."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 3000)
+    pr, g, o = run_both(ctx, orc, cfg)
+    assert g["stats"]["matmul_path"] == 2
+    cfg0 = synth.scaled(synth.CONFIGS["C0"], 256)       # max|xs|^2 > 16 -> guard
+    pr, g, o = run_both(ctx, orc, cfg0)
+    assert g["stats"]["matmul_path"] == 0
+    cfg2 = synth.scaled(synth.CONFIGS["C2"], 500)       # Matern -> CUDA-core path
+    pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
+    assert g["stats"]["matmul_path"] == 0
 
 
 def test_tiny_problem(ctx, orc):
