@@ -88,6 +88,15 @@ for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_c
     getattr(_lib, _f).restype = C.c_int
 
 
+def row_partition(n: int, nranks: int, rank: int):
+    """Rows [r0, r1) owned by `rank` (mirrors bbmm_local_rows): blocks of
+    nb = ceil(ceil(n / nranks) / 128) * 128 rows, so rank boundaries align with
+    the 128-point j-tiles of the tensor-core operand and the all-gathers."""
+    nb = -(-(-(-n // nranks)) // 128) * 128
+    r0 = min(n, rank * nb)
+    return r0, min(n, r0 + nb), nb
+
+
 def version() -> str:
     return _lib.bbmm_version().decode()
 
