@@ -161,6 +161,44 @@ __global__ void k_scalar_terms(const double *__restrict__ U, const double *__res
     }
 }
 
+// Derivative-pass operand for the tensor-core path: Bd = [Z0_1..Z0_t / t, -u0] (fp64).
+__global__ void k_build_bd(const double *__restrict__ U, const double *__restrict__ Z0,
+                           int64_t nloc, int t, double *__restrict__ Bd) {
+    const int c = t + 1;
+    const double inv_t = 1.0 / (double)t;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * c;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / c;
+        const int col = (int)(e - i * c);
+        Bd[e] = col < t ? Z0[i * c + 1 + col] * inv_t : -U[i * c];
+    }
+}
+
+// part[blk] = sum over this block's rows a of A_a . V_a, V = sum of split partials,
+// A_a = [u_1..u_t, u_0](a) (so that sum_a A_a . (dK B)_a = S = tau - quad).
+__global__ void k_deriv_dot(const double *__restrict__ Vpart, int splits, int cs, int64_t nloc,
+                            int t, const double *__restrict__ U, double *__restrict__ part) {
+    const int c = t + 1;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        for (int col = 0; col < c; col++) {
+            double v = 0.0;
+            for (int s = 0; s < splits; s++) v += Vpart[((int64_t)s * nloc + i) * cs + col];
+            const double av = col < t ? U[i * c + 1 + col] : U[i * c];
+            acc += av * v;
+        }
+    }
+    __shared__ double sh[256];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int u = 0; u < (int)blockDim.x; u++) s += sh[u];
+        part[blockIdx.x] = s;
+    }
+}
+
 __global__ void k_check_finite(const float *__restrict__ x, int64_t n, int *bad) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -506,29 +544,64 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         Timer t_slq(sm);
 
         // 5. derivative pass (once)
-        float *A32 = (float *)ws.get("A32", (size_t)std::max<int64_t>(nloc, 1) * cs * 4);
-        float *B32 = (float *)ws.get("B32", (size_t)rr.nb * ctx->nranks * cs * 4);
-        BBMM_CUDA(cudaMemsetAsync(B32, 0, (size_t)rr.nb * ctx->nranks * cs * 4, sm));
-        if (nloc > 0) {
-            k_pack_deriv<<<grid_for(nloc * cs), 256, 0, sm>>>(o.U_d, Z0, nloc, t, cs, rr.r0, A32,
-                                                             B32);
-            ctx->launches++;
-        }
-        allgather_rows(ctx, B32, (size_t)rr.nb * cs * 4);
         const int nq = dp + 1;
-        double *dpart = (double *)ws.get("d_part", derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp) * 8);
         double *dred = (double *)ws.get("d_red", (size_t)(nq + 3) * 8);
         BBMM_CUDA(cudaMemsetAsync(dred, 0, (size_t)(nq + 3) * 8, sm));
         const int sblk = grid_for(std::max<int64_t>(nloc, 1));
         double *spart = (double *)ws.get("s_part", (size_t)sblk * 3 * 8);
-        if (nloc > 0) {
-            int nblk = 0;
-            derivative_pass(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, nq, h.n_ls > 1, d,
-                            dpart, &nblk);
-            reduce_blocks(ctx, dpart, nblk, nq, dred);
-            k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
-            ctx->launches++;
-            reduce_blocks(ctx, spart, sblk, 3, dred + nq);
+        const bool tc_deriv = tcop.version == 2 && k1tc2_deriv_supported(h.kind, h.n_ls, d, c);
+        if (tc_deriv) {
+            // isotropic RBF: S_l = sum_a A_a . (s K~ o R^2 B)_a, S_s = sum_a A_a . (s K~ B)_a,
+            // two exact tensor-core kernel-matmuls of the packed B = [P^-1 Z / t | -u0]
+            double *Bd = (double *)ws.get("d_Bd", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
+            double *Sd = (double *)ws.get("d_S", kMaxCols * 8);
+            const int64_t npad_tc = k1tc_pad_rows(rr.nb * ctx->nranks);
+            uint8_t *Bp = (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(c));
+            if (nloc > 0) {
+                k_build_bd<<<grid_for(nloc * c), 256, 0, sm>>>(o.U_d, Z0, nloc, t, Bd);
+                ctx->launches++;
+            }
+            k1tc_colmax(ctx, Bd, c, nloc, c, Sd);
+            allreduce_max(ctx, Sd, c);
+            if (nloc > 0) k1tc_pack(ctx, Bd, c, rr.r0, nloc, n, c, Sd, Bp);
+            allgather_rows(ctx, Bp, (size_t)rr.nb * k1tc_bslice_rows(c));
+            const size_t cap = tc_vpart_elems(tcop, n, nloc, c);
+            double *Vp = (double *)ws.get("d_Vpart", std::max<size_t>(cap, 1) * 8);
+            double *dpart = (double *)ws.get("d_part", (size_t)sblk * 8);
+            for (int mode = 0; mode < 2 && nloc > 0; mode++) {
+                const int sp = tc_matmul(ctx, tcop, Bp, Sd, c, n, rr.r0, nloc, h.s, Vp, cap,
+                                         nullptr, nullptr, mode);
+                k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, (c + 3) & ~3, nloc, t, o.U_d, dpart);
+                ctx->launches++;
+                // mode 1 -> S_l at dred[0]; mode 0 -> S_s at dred[dp]
+                reduce_blocks(ctx, dpart, sblk, 1, dred + (mode == 1 ? 0 : dp));
+            }
+            if (nloc > 0) {
+                k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
+                ctx->launches++;
+                reduce_blocks(ctx, spart, sblk, 3, dred + nq);
+            }
+        } else {
+            float *A32 = (float *)ws.get("A32", (size_t)std::max<int64_t>(nloc, 1) * cs * 4);
+            float *B32 = (float *)ws.get("B32", (size_t)rr.nb * ctx->nranks * cs * 4);
+            BBMM_CUDA(cudaMemsetAsync(B32, 0, (size_t)rr.nb * ctx->nranks * cs * 4, sm));
+            if (nloc > 0) {
+                k_pack_deriv<<<grid_for(nloc * cs), 256, 0, sm>>>(o.U_d, Z0, nloc, t, cs, rr.r0,
+                                                                 A32, B32);
+                ctx->launches++;
+            }
+            allgather_rows(ctx, B32, (size_t)rr.nb * cs * 4);
+            double *dpart = (double *)ws.get(
+                "d_part", derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp) * 8);
+            if (nloc > 0) {
+                int nblk = 0;
+                derivative_pass(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, nq, h.n_ls > 1,
+                                d, dpart, &nblk);
+                reduce_blocks(ctx, dpart, nblk, nq, dred);
+                k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
+                ctx->launches++;
+                reduce_blocks(ctx, spart, sblk, 3, dred + nq);
+            }
         }
         allreduce_sum(ctx, dred, (size_t)nq + 3);
         BBMM_LAUNCH_CHECK();
@@ -546,16 +619,22 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         const double logdet = hs[0] + hs[1];
         const double quad_y = hred[nq + 0], uu = hred[nq + 1], uz = hred[nq + 2];
         *mll_h = -0.5 * (quad_y + logdet + (double)n * std::log(2.0 * M_PI));
-        // lengthscale / outputscale components: grad = -S/2 with constants
-        const double lfac = (h.kind == BBMM_RBF) ? h.s * 2.0 * std::log(2.0) : h.s / 3.0;
-        if (h.n_ls == 1) {
-            double sl = 0.0;
-            for (int q = 0; q < d; q++) sl += hred[q];
-            grad_h[0] = -0.5 * lfac * sl;
+        // lengthscale / outputscale components: grad = -S/2
+        if (tc_deriv) {
+            grad_h[0] = -0.5 * hred[0];          // S_l (includes s)
+            grad_h[1] = -0.5 * hred[dp];         // S_s (includes s)
         } else {
-            for (int q = 0; q < d; q++) grad_h[q] = -0.5 * lfac * hred[q];
+            // CUDA-core pass accumulates per input dimension in scaled units
+            const double lfac = (h.kind == BBMM_RBF) ? h.s * 2.0 * std::log(2.0) : h.s / 3.0;
+            if (h.n_ls == 1) {
+                double sl = 0.0;
+                for (int q = 0; q < d; q++) sl += hred[q];
+                grad_h[0] = -0.5 * lfac * sl;
+            } else {
+                for (int q = 0; q < d; q++) grad_h[q] = -0.5 * lfac * hred[q];
+            }
+            grad_h[h.n_ls] = -0.5 * h.s * hred[dp];
         }
-        grad_h[h.n_ls] = -0.5 * h.s * hred[dp];
         // log sigma: dKhat = 2 sigma^2 I
         const double tau_s = 2.0 * h.noise_var * uz / (double)t;
         const double quad_s = 2.0 * h.noise_var * uu;

@@ -152,7 +152,8 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
 size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c);
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                  const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
-                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1);
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0);
+bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c);
 
 // Tensor-core operand of one mBCG call (prepared once per call).
 struct TcOperand {
@@ -167,7 +168,7 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
 size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c);
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
-              cudaEvent_t ev0, cudaEvent_t ev1);
+              cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0);
 
 // ------------------------------------------------------- pivchol.cu
 void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, int k,

@@ -93,7 +93,9 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, int nb, int off1, 
     }
 }
 
-template <int C, int DA>
+// MODE 0: value k~ = K/s (the blackbox matmul);  MODE 1: value k~ r^2
+// (= (dK/dlog l)/s for the isotropic RBF, used by the derivative pass).
+template <int C, int DA, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
           const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
@@ -256,7 +258,11 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 uint32_t q[4];
 #pragma unroll
                 for (int v = 0; v < 4; v++) {
-                    const float kv = ex2_approx(__uint_as_float(sv[4 * u + v]));
+                    const float sj = __uint_as_float(sv[4 * u + v]);
+                    float kv = ex2_approx(sj);
+                    // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
+                    // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
+                    if (MODE == 1) kv *= fmaxf(-1.3862943611198906f * sj, 0.0f);
                     q[v] = __float_as_uint(fmaf(kv, 0.5f, 1.0f));
                 }
                 const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
@@ -392,7 +398,7 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
     return mf;
 }
 
-template <int C, int DA>
+template <int C, int DA, int MODE>
 static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                       const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
                       double *Vpart, size_t cap) {
@@ -405,13 +411,13 @@ static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const u
     BBMM_REQUIRE((size_t)sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k1tc2)");
     static bool attr = false;
     if (!attr) {
-        BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA>,
+        BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)rb, (unsigned)sp);
-    tc2::k1tc2_rbf<C, DA><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(Xa, XB, Bp, S, r0, nloc,
-                                                                         tps, ntiles, s, Vpart);
+    tc2::k1tc2_rbf<C, DA, MODE><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(
+        Xa, XB, Bp, S, r0, nloc, tps, ntiles, s, Vpart);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
     return (int)sp;
@@ -424,14 +430,30 @@ size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c) {
     return (size_t)sp * std::max<int64_t>(nloc, 1) * ((c + 3) & ~3);
 }
 
+bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c) {
+    return n_ls == 1 && (c == 11 || c == 17) && k1tc2_supported(kind, d, c);
+}
+
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                  const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
-                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1) {
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
     if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
     int sp = 1;
     const int da = tc2_da(d);
+    if (mode == 1) {
+        BBMM_REQUIRE(k1tc2_deriv_supported(BBMM_RBF, 1, d, c), "k1tc2: derivative mode shape");
+        if (nloc > 0) {
+            if (c == 11 && da == 8) sp = launch_tc2<11, 8, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 11 && da == 24) sp = launch_tc2<11, 24, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported derivative shape"};
+        }
+        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        return sp;
+    }
 #define BBMM_TC2(CC, DD) \
-    if (c == CC && da == DD) sp = launch_tc2<CC, DD>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+    if (c == CC && da == DD) sp = launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
     if (nloc > 0) {
         BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
         BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)
@@ -473,8 +495,9 @@ size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c) {
 
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
-              cudaEvent_t ev0, cudaEvent_t ev1) {
-    return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1);
+              cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
+    return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1,
+                        mode);
 }
 
 }  // namespace bbmm
