@@ -118,7 +118,9 @@ void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *me
     ctx->launches++;
 }
 
-int64_t k1tc_pad_rows(int64_t n) { return ceil_div(n, 128) * 128; }   // covers both tile widths
+// rows covered by the tensor-core operands: a multiple of 384 = lcm(128-row
+// partitions, 96-point j-tiles)
+int64_t k1tc_pad_rows(int64_t n) { return ceil_div(n, 384) * 384; }
 
 // S (c doubles, device): column max |D| over the rows given (local rows);
 // caller all-reduces (max) across ranks if needed.
@@ -136,10 +138,12 @@ void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, in
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
                int64_t n, int c, const double *S, uint8_t *Bpack) {
     const int C1 = c + 1, NB = tc::round16(4 * C1);
-    // cover the rows up to the next multiple of 128 (the widest j-tile any
-    // consumer reads); rows >= n are written as zeros
+    // the rank holding the last rows also writes the zero padding up to
+    // k1tc_pad_rows(n) (the j-tiles read past n); the layout is linear in
+    // 16-point chunks, [chunk][NB][16 B], so any tile width reads it
+    const int64_t end = (row0 + rows >= n) ? k1tc_pad_rows(n) : row0 + rows;
     const int64_t tile0 = row0 / tc::BK;
-    const int64_t tiles = ceil_div(ceil_div(row0 + rows, 128) * 128, tc::BK) - tile0;
+    const int64_t tiles = ceil_div(end, tc::BK) - tile0;
     const int64_t total = tiles * (tc::BK / 16) * NB;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
     tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, C1, NB, S, Bpack,

@@ -14,13 +14,13 @@
 // Per pair a compute thread then issues ~5 instructions (ex2, 1 FFMA,
 // byte permutes) so the kernel is bound by the MUFU ex2 pipe.
 //
-// CTA = 128 rows, 1 CTA per SM, 19 warps:
+// CTA = 128 rows, 1 CTA per SM, 18 warps:
 //   warps 0-15: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
 //               h = w / 4 (16 of the 64 j) of every j tile
 //   warp 16   : producer (bulk copies of the B' distance tile and the packed
 //               D slices)
-//   warp 17   : MMA issuer for the int8 contraction of tile t
-//   warp 18   : MMA issuer for the distance MMAs (runs up to 2 tiles ahead)
+//   warp 17   : MMA issuer: int8 contraction of tile t, then the distance
+//               MMA of tile t + NBUF into the TMEM buffer just consumed
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -34,15 +34,17 @@ namespace bbmm {
 namespace tc2 {
 
 // j-tile BK = 128; 16 compute warps, warp (sub, h) serves TMEM lanes
-// 32 sub.. and the j-group h (32 j) of every tile.  Each TMEM stage buffer
-// (128 columns) first receives S (fp32, from the distance MMA); every warp
-// then overwrites ITS OWN 32 S columns with the three int8 slices of its
-// quantised kernel values (24 columns), which the int8 MMAs read as A.
-constexpr int BM = 128, BK = 128, STAGES = 3, NBUF = 2;
-constexpr int WINDOW = 16384;
-constexpr int NQ = 4, JW = BK / NQ, NCW = 4 * NQ;
-constexpr int kThreads = 32 * (NCW + 3);
-constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1, DIST_WARP = NCW + 2;
+// 32 sub.. and the j-group h (32 j) of every tile.  Each of the NBUF = 2 TMEM
+// buffers (128 columns) first receives S (fp32, from the distance MMA); every
+// warp then overwrites ITS OWN 32 S columns with the three int8 slices of
+// its quantised kernel values (24 columns), which the int8 MMAs read as A.
+// (Measured: BK = 96 with 3 buffers and 12 warps is slower -- fewer warps
+// per scheduler hide less MUFU/TMEM latency.)
+constexpr int BM = 128, BK = 128, NBUF = 2, STAGES = NBUF + 1;
+constexpr int NQ = BK / 32, JW = BK / NQ, NCW = 4 * NQ;
+constexpr int WINDOW = BK * (16384 / BK);    // j per TMEM drain, <= 32768 (int32 bound)
+constexpr int kThreads = 32 * (NCW + 2);
+constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(JW == 32, "one 32-column group per warp");
 constexpr __host__ __device__ int r16(int x) { return (x + 15) & ~15; }
 constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
@@ -53,15 +55,16 @@ struct Cfg {
     static constexpr int NB = r16(4 * C1), NQ1 = r16(3 * C1), NQ0 = r16(2 * C1);
     static constexpr int OFF1 = r32(NB), OFF0 = OFF1 + r32(NQ1);
     static constexpr int ACC_END = OFF0 + r32(NQ0);
-    static constexpr int AP_OFF = ACC_END;                     // 3 DA tf32 columns
-    static constexpr int BUF_OFF = r32(AP_OFF + 3 * DA);       // NBUF x BK columns
+    static constexpr int BUF_OFF = ACC_END;                    // NBUF x BK columns
     static constexpr int END = BUF_OFF + NBUF * BK;
     static_assert(END <= 512, "TMEM budget exceeded");
     static constexpr int B8_BYTES = NB * BK;                   // int8 D slices per tile
     static constexpr int XB_BYTES = 3 * DA * BK * 4;           // tf32 B' per tile
     static constexpr int STAGE_BYTES = B8_BYTES + XB_BYTES;
+    static constexpr int AP_BYTES = BM * 3 * DA * 4;           // row operand A' (smem)
+    static constexpr int RAW = STAGES * STAGE_BYTES + AP_BYTES + 1024;
     // >= 120 KB so that a single CTA (which owns all 512 TMEM columns) is resident per SM
-    static constexpr int SMEM = (STAGES * STAGE_BYTES + 1024) > 122880 ? (STAGES * STAGE_BYTES + 1024) : 122880;
+    static constexpr int SMEM = RAW > 122880 ? RAW : 122880;
 };
 
 // Drain one window's int32 accumulators of this thread's row (TMEM lane)
@@ -106,7 +109,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full_b[STAGES], free_b[STAGES];
-    __shared__ __align__(8) uint64_t s_full[NBUF], a_full[NBUF], buf_free[NBUF];
+    __shared__ __align__(8) uint64_t s_full[NBUF], a_full[NBUF];
     __shared__ __align__(8) uint64_t acc_full, acc_empty, init_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ double acc_sm[C + 1][BM];   // fp64 accumulators (+ constant column)
@@ -125,7 +128,6 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         for (int q = 0; q < NBUF; q++) {
             ptx::mbar_init(&s_full[q], 1);
             ptx::mbar_init(&a_full[q], 32 * NCW);
-            ptx::mbar_init(&buf_free[q], 1);
         }
         ptx::mbar_init(&acc_full, 1);
         ptx::mbar_init(&acc_empty, 128);
@@ -155,35 +157,37 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             }
             __syncwarp();
         }
-    } else if (warp == DIST_WARP) {
-        // ----------------------------------- MMA issuer: distance S = A'.B'
-        constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
-        const bool leader = ptx::elect_one();
-        ptx::mbar_wait(&init_done, 0);
-        for (int t = 0; t < ntl; t++) {
-            const int st = t % STAGES;
-            const int b = t % NBUF;
-            ptx::mbar_wait(&full_b[st], (uint32_t)((t / STAGES) & 1));
-            ptx::mbar_wait(&buf_free[b], (uint32_t)(((t / NBUF) & 1) ^ 1));
-            ptx::tc_fence_after();
-            if (leader) {
-                const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
-#pragma unroll
-                for (int ks = 0; ks < 3 * DA / 8; ks++) {
-                    const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
-                    ptx::mma_tf32_ts(tmem + K::BUF_OFF + b * BK, tmem + K::AP_OFF + ks * 8, bd, IDS,
-                                     ks > 0 ? 1u : 0u);
-                }
-                ptx::mma_commit(&s_full[b]);
-            }
-            __syncwarp();
-        }
     } else if (warp == MMA_WARP) {
-        // ---------------------------- MMA issuer: exact int8 contraction
+        // ------------------------------------------------------ MMA issuer
+        // One thread issues both MMA kinds.  tcgen05.mma ops of one thread
+        // execute in issue order, so the distance MMA of tile t + NBUF, issued
+        // right after the int8 MMAs of tile t that read the same TMEM buffer,
+        // cannot overwrite it early: no buffer-free round trip is needed.
+        constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
         constexpr uint32_t ID2 = ptx::idesc_i8(BM, K::NB, false, false);
         constexpr uint32_t ID1 = ptx::idesc_i8(BM, K::NQ1, false, false);
         constexpr uint32_t ID0 = ptx::idesc_i8(BM, K::NQ0, false, false);
         const bool leader = ptx::elect_one();
+        ptx::mbar_wait(&init_done, 0);
+        auto issue_dist = [&](int t) {
+            const int st = t % STAGES;
+            const int b = t % NBUF;
+            ptx::mbar_wait(&full_b[st], (uint32_t)((t / STAGES) & 1));
+            ptx::tc_fence_after();
+            if (leader) {
+                const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
+                const uint32_t ap = ptx::smem_u32(smem + STAGES * K::STAGE_BYTES);
+#pragma unroll
+                for (int ks = 0; ks < 3 * DA / 8; ks++) {
+                    const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
+                    const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
+                    ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&s_full[b]);
+            }
+            __syncwarp();
+        };
+        for (int t = 0; t < NBUF && t < ntl; t++) issue_dist(t);
         for (int t = 0; t < ntl; t++) {
             const int st = t % STAGES;
             const int b = t % NBUF;
@@ -203,11 +207,11 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     ptx::mma_i8_ts(tmem + K::OFF1, aq + 32 * ks + 8, bd, ID1, acc);  // q1
                     ptx::mma_i8_ts(tmem + K::OFF0, aq + 32 * ks + 0, bd, ID0, acc);  // q0
                 }
-                ptx::mma_commit(&buf_free[b]);
                 ptx::mma_commit(&free_b[st]);
                 if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
             }
             __syncwarp();
+            if (t + NBUF < ntl) issue_dist(t + NBUF);
         }
     } else {
         // -------------------------------------------------------- compute
@@ -216,28 +220,25 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const bool valid = row < nloc;
         const uint32_t lane_base = tmem + ((uint32_t)(sub * 32) << 16);
         if (h == 0) {
-            // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32)
-            uint32_t hi[DA], lo[DA];
+            // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32), written to
+            // shared memory K-major: [3 DA / 4 chunks][128 rows][4 floats]
+            const int rl = sub * 32 + lane;
+            float *ap = reinterpret_cast<float *>(smem + STAGES * K::STAGE_BYTES);
 #pragma unroll
             for (int q = 0; q < DA; q++) {
                 const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
-                const uint32_t vb = __float_as_uint(v) & 0xFFFFE000u;
-                hi[q] = vb;
-                lo[q] = __float_as_uint(v - __uint_as_float(vb));
-            }
+                const float vh = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                const float vl = v - vh;
+                const float parts[3] = {vh, vh, vl};
 #pragma unroll
-            for (int q0 = 0; q0 < DA; q0 += 8) {
-                uint32_t a8[8], b8[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) { a8[u] = hi[q0 + u]; b8[u] = lo[q0 + u]; }
-                ptx::tmem_st8(lane_base + K::AP_OFF + q0, a8);
-                ptx::tmem_st8(lane_base + K::AP_OFF + DA + q0, a8);
-                ptx::tmem_st8(lane_base + K::AP_OFF + 2 * DA + q0, b8);
+                for (int pt = 0; pt < 3; pt++) {
+                    const int k = pt * DA + q;
+                    ap[(k >> 2) * (BM * 4) + rl * 4 + (k & 3)] = parts[pt];
+                }
             }
-            ptx::tmem_st_wait();
-            ptx::tc_fence_before();
+            ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&init_done);
-            for (int c = 0; c <= C; c++) acc_sm[c][sub * 32 + lane] = 0.0;
+            for (int c = 0; c <= C; c++) acc_sm[c][rl] = 0.0;
         }
         const uint32_t a_sfull = ptx::smem_u32(&s_full[0]);
         const uint32_t a_afull = ptx::smem_u32(&a_full[0]);

@@ -86,21 +86,48 @@ __global__ void k_init_vectors(const double *__restrict__ B, int64_t ldb, int64_
 }
 
 // W partial = L^T R over this block's rows: part[blk][m*c + col].
-// Thread (col, y): loops over m = y, y + rb, ... (m < k), over the block's rows.
-__global__ void k_LtR(const double *__restrict__ L, int64_t n, int64_t r0, int k,
-                      const double *__restrict__ R, int64_t nloc, int c,
-                      double *__restrict__ part) {
-    const int col = threadIdx.x;
-    const int64_t rows_per_blk = ceil_div(nloc, (int64_t)gridDim.x);
-    const int64_t i0 = (int64_t)blockIdx.x * rows_per_blk;
-    const int64_t i1 = min(nloc, i0 + rows_per_blk);
-    for (int m = threadIdx.y; m < k; m += blockDim.y) {
-        if (col >= c) continue;
-        const double *Lm = L + (int64_t)m * n + r0;
-        double acc = 0.0;
-        for (int64_t i = i0; i < i1; i++) acc += Lm[i] * R[i * c + col];
-        part[(int64_t)blockIdx.x * k * c + (int64_t)m * c + col] = acc;
+// Block = 256 threads (8 warps); a 256-row tile of R is staged in shared
+// memory; for each m every thread forms L[m][row] R[row][:] for its row
+// (coalesced L reads), warps reduce over their 32 rows with shuffles, and the
+// 8 warp partials are added in a fixed order into a per-block k x c
+// accumulator (deterministic).  Grid-stride over row tiles.
+constexpr int kLtrRows = 256;
+__global__ void __launch_bounds__(256)
+k_LtR(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *__restrict__ R,
+      int64_t nloc, int c, double *__restrict__ part) {
+    extern __shared__ double sm_ltr[];
+    double *Rt = sm_ltr;                          // kLtrRows x c
+    double *wp = Rt + kLtrRows * c;               // 8 warps x c
+    double *acc = wp + 8 * c;                     // k x c block accumulator
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < k * c; e += 256) acc[e] = 0.0;
+    for (int64_t i0 = (int64_t)blockIdx.x * kLtrRows; i0 < nloc;
+         i0 += (int64_t)gridDim.x * kLtrRows) {
+        __syncthreads();
+        for (int e = tid; e < kLtrRows * c; e += 256) {
+            const int64_t i = i0 + e / c;
+            Rt[e] = i < nloc ? R[i0 * c + e] : 0.0;
+        }
+        __syncthreads();
+        const int64_t i = i0 + tid;
+        for (int mm = 0; mm < k; mm++) {
+            const double l = i < nloc ? L[(int64_t)mm * n + r0 + i] : 0.0;
+            for (int col = 0; col < c; col++) {
+                double v = l * Rt[tid * c + col];
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) wp[warp * c + col] = v;
+            }
+            __syncthreads();
+            for (int col = tid; col < c; col += 256) {
+                double s = 0.0;
+                for (int w = 0; w < 8; w++) s += wp[w * c + col];
+                acc[mm * c + col] += s;
+            }
+            __syncthreads();
+        }
     }
+    __syncthreads();
+    for (int e = tid; e < k * c; e += 256) part[(int64_t)blockIdx.x * k * c + e] = acc[e];
 }
 
 // S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One block,
@@ -120,34 +147,58 @@ __device__ void chol_solve_col(const double *__restrict__ cholC, int k, const do
 }
 
 // Z = (R - L S)/sigma^2  (k >= 1) or Z = R (no preconditioner); partial <R,Z>.
-__global__ void k_precond_apply(const double *__restrict__ L, int64_t n, int64_t r0, int k,
-                                const double *__restrict__ S, double noise_var,
-                                const double *__restrict__ R, int64_t nloc, int c,
-                                double *__restrict__ Z, double *__restrict__ part) {
-    extern __shared__ double Ssm[];   // k x c
-    for (int e = threadIdx.y * blockDim.x + threadIdx.x; e < k * c; e += blockDim.x * blockDim.y)
-        Ssm[e] = S[e];
+// Thread = one row x a chunk of 8 columns (blockIdx.y): L[m][row] loads are
+// coalesced across the warp, S comes from shared memory (broadcast).  The
+// per-column partials are reduced warp -> block in a fixed order.
+__global__ void __launch_bounds__(256)
+k_precond_apply(const double *__restrict__ L, int64_t n, int64_t r0, int k,
+                const double *__restrict__ S, double noise_var, const double *__restrict__ R,
+                int64_t nloc, int c, double *__restrict__ Z, double *__restrict__ part) {
+    extern __shared__ double Ssm[];   // k x c, then 8 x 8 warp partials
+    double *wp = Ssm + k * c;
+    for (int e = threadIdx.x; e < k * c; e += blockDim.x) Ssm[e] = S[e];
     __syncthreads();
-    const int col = threadIdx.x;
-    double acc = 0.0;
-    if (col < c) {
-        const double inv = 1.0 / noise_var;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; i < nloc;
-             i += (int64_t)gridDim.x * blockDim.y) {
-            double r = R[i * c + col];
-            double z;
-            if (k > 0) {
-                double ls = 0.0;
-                for (int m = 0; m < k; m++) ls += L[(int64_t)m * n + r0 + i] * Ssm[m * c + col];
-                z = (r - ls) * inv;
-            } else {
-                z = r;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = blockIdx.y * 8;
+    const double inv = 1.0 / noise_var;
+    double rz[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) rz[u] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + tid; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = 0.0;
+        if (k > 0) {
+            for (int mm = 0; mm < k; mm++) {
+                const double l = L[(int64_t)mm * n + r0 + i];
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (c0 + u < c) acc[u] += l * Ssm[mm * c + c0 + u];
             }
-            Z[i * c + col] = z;
-            acc += r * z;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (c0 + u < c) {
+                const double r = R[i * c + c0 + u];
+                const double z = k > 0 ? (r - acc[u]) * inv : r;
+                Z[i * c + c0 + u] = z;
+                rz[u] += r * z;
+            }
         }
     }
-    block_reduce_cols(acc, part, c, 0);
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        double v = rz[u];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) wp[warp * 8 + u] = v;
+    }
+    __syncthreads();
+    if (tid < 8 && c0 + tid < c) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += wp[w * 8 + tid];
+        part[(int64_t)blockIdx.x * c + c0 + tid] = s;
+    }
 }
 
 // Initial state after R = B, Z = P^{-1} B.  red: [bb (c) | rz (c)].
@@ -490,7 +541,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     BBMM_CUDA(cudaMemsetAsync(ahist, 0, (size_t)a.max_iter * c * 8, sm));
     BBMM_CUDA(cudaMemsetAsync(bhist, 0, (size_t)a.max_iter * c * 8, sm));
     BBMM_CUDA(cudaMemsetAsync(Dm, 0, (size_t)npad * cs * esz, sm));
-    const size_t smem_S = (size_t)kk * c * 8;
+    const size_t smem_S = (size_t)kk * c * 8 + 64 * 8;
     if (smem_S > 48 * 1024)
         BBMM_CUDA(cudaFuncSetAttribute(k_precond_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_S));
@@ -502,10 +553,26 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         launches++;
     };
     // W = L^T R (+ |R|^2 already in red[0..c) when with_rr) -> red[c..c+kc)
+    const int ltr_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kLtrRows),
+                                                                        2 * kNumSMs));
+    const size_t smem_ltr = ((size_t)kLtrRows * c + 8 * c + (size_t)kk * c) * 8;
+    if (smem_ltr > 48 * 1024)
+        BBMM_CUDA(cudaFuncSetAttribute(k_LtR, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_ltr));
+    double *part_ltr = (double *)ws.get("cg_part_ltr", (size_t)ltr_blocks * kk * c * 8);
     auto LtR = [&](double *dst) {
         if (k == 0) return;
-        k_LtR<<<g.grid, g.block, 0, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part);
-        reduce(k * c, dst);
+        k_LtR<<<ltr_blocks, 256, smem_ltr, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part_ltr);
+        k_reduce_blocks<<<std::max(1, (int)ceil_div(k * c, 256)), 256, 0, sm>>>(
+            part_ltr, ltr_blocks, k * c, dst);
+        launches += 2;
+    };
+    // precondition apply: grid (row blocks, column chunks of 8); partials nblk x c
+    const dim3 pa_grid((unsigned)nblk, (unsigned)ceil_div(c, 8));
+    auto precond_apply = [&](double *dst) {
+        k_precond_apply<<<pa_grid, 256, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R, nloc,
+                                                      c, Z, part);
+        reduce(c, dst);
         launches++;
     };
 
@@ -520,10 +587,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         launches++;
     }
     double *red_rz = red + (size_t)(kk + 1) * c;
-    k_precond_apply<<<g.grid, g.block, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R, nloc, c,
-                                                     Z, part);
-    launches++;
-    reduce(c, red_rz);
+    precond_apply(red_rz);
     if (multi) allreduce_sum(ctx, red_rz, c);
     k_init_state<<<1, 64, 0, sm>>>(st, red, red_rz, c);
     launches++;
@@ -585,9 +649,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         LtR(red + c);
         if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
         k_after_B<<<1, 64, 0, sm>>>(st, red, cholC, k, c, a.tol, S);
-        k_precond_apply<<<g.grid, g.block, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R,
-                                                         nloc, c, Z, part);
-        reduce(c, red_rz);
+        precond_apply(red_rz);
         if (multi) allreduce_sum(ctx, red_rz, c);
         k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
         launches += 7;
