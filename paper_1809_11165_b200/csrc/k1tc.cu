@@ -63,13 +63,13 @@ __global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c,
     S[col] = m > 0.0 ? m : 1.0;
 }
 
-// Pack rows [row0, row0 + rows) of D (fp64) into the per-tile K-major slice
-// layout: tile tt = j / BK holds NB rows (n = b_idx * C1 + col; b_idx 0..3 =
-// bytes 3..0 of P' = round(D/S 2^30) + 2^30; col == C is the constant 2^30)
-// of BK bytes, as [BK/16 chunks][NB rows][16 bytes].  One thread writes the
-// 16 bytes of one (tile, chunk, n).
+// Pack rows [row0, row0 + rows) of D (fp64) into the K-major slice layout
+// [16-point chunk][NB rows][16 bytes] (linear in the chunk index, so any
+// multiple-of-16 j-tile is contiguous): row n = b_idx * BLK + col, b_idx 0..3
+// = bytes 3..0 of P' = round(D/S 2^30) + 2^30, col == c is the constant 2^30,
+// col > c zero padding.  One thread writes the 16 bytes of one (chunk, n).
 __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_t row0,
-                               int64_t rows, int64_t n, int c, int C1, int NB,
+                               int64_t rows, int64_t n, int c, int BLK, int NB,
                                const double *__restrict__ S, uint8_t *__restrict__ Bpack,
                                int64_t tile0, int64_t tiles) {
     const int64_t total = tiles * (BK / 16) * NB;
@@ -79,9 +79,9 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
         const int64_t rest = e / NB;
         const int kc = (int)(rest % (BK / 16));
         const int64_t tt = tile0 + rest / (BK / 16);
-        const int bi = nn / C1, col = nn - bi * C1;
+        const int bi = nn / BLK, col = nn - bi * BLK;
         uint32_t wv[4] = {0, 0, 0, 0};
-        if (bi < 4) {
+        if (bi < 4 && col <= c) {
             const int shift = 8 * (3 - bi);
 #pragma unroll
             for (int p = 0; p < 16; p++) {
@@ -110,7 +110,9 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
 // ======================================================================
 // host side
 // ======================================================================
-int k1tc_bslice_rows(int c) { return tc::round16(4 * (c + 1)); }
+// rows of the packed D-slice operand: 4 blocks of BLK >= c + 1 columns
+// (BLK in {16, 32, 48}, matching k1tc2's accumulator blocks)
+int k1tc_bslice_rows(int c) { return 4 * (c + 1 <= 16 ? 16 : (c + 1 <= 32 ? 32 : 48)); }
 
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean) {
     tc::k_col_mean<<<d, 256, 0, ctx->stream>>>(X, n, d, mean);
@@ -137,7 +139,7 @@ void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, in
 // Pack local rows [row0, row0 + rows) into Bpack (tiles covering them).
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
                int64_t n, int c, const double *S, uint8_t *Bpack) {
-    const int C1 = c + 1, NB = tc::round16(4 * C1);
+    const int NB = k1tc_bslice_rows(c), BLK = NB / 4;
     // the rank holding the last rows also writes the zero padding up to
     // k1tc_pad_rows(n) (the j-tiles read past n); the layout is linear in
     // 16-point chunks, [chunk][NB][16 B], so any tile width reads it
@@ -146,7 +148,7 @@ void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int6
     const int64_t tiles = ceil_div(end, tc::BK) - tile0;
     const int64_t total = tiles * (tc::BK / 16) * NB;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
-    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, C1, NB, S, Bpack,
+    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, BLK, NB, S, Bpack,
                                                       tile0, tiles);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;

@@ -34,27 +34,38 @@ namespace bbmm {
 namespace tc2 {
 
 // j-tile BK = 128; 16 compute warps, warp (sub, h) serves TMEM lanes
-// 32 sub.. and the j-group h (32 j) of every tile.  Each of the NBUF = 2 TMEM
-// buffers (128 columns) first receives S (fp32, from the distance MMA); every
-// warp then overwrites ITS OWN 32 S columns with the three int8 slices of
-// its quantised kernel values (24 columns), which the int8 MMAs read as A.
-// (Measured: BK = 96 with 3 buffers and 12 warps is slower -- fewer warps
-// per scheduler hide less MUFU/TMEM latency.)
-constexpr int BM = 128, BK = 128, NBUF = 2, STAGES = NBUF + 1;
+// 32 sub.. and the j-group h (32 j) of every tile.  Each of the NBUF TMEM
+// buffers (128 columns; NBUF = 3 when the accumulators take <= 128 columns)
+// first receives S (fp32, from the distance MMA); every warp then overwrites
+// ITS OWN 32 S columns with the three int8 slices of its quantised kernel
+// values (24 columns), which the int8 MMAs read as A.  With three buffers
+// the MMA side runs two tiles ahead of the slowest warp.
+constexpr int BM = 128, BK = 128;
 constexpr int NQ = BK / 32, JW = BK / NQ, NCW = 4 * NQ;
-constexpr int WINDOW = BK * (16384 / BK);    // j per TMEM drain, <= 32768 (int32 bound)
+// j per TMEM drain: an accumulator column gathers up to 3 slice products of
+// <= 255 x 255 per j, so int32 is safe for < 2^31 / 195075 = 11008 j
+constexpr int WINDOW = 8192;
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(JW == 32, "one 32-column group per warp");
 constexpr __host__ __device__ int r16(int x) { return (x + 15) & ~15; }
 constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
 
+// Accumulator layout: the slice products are merged by weight.  The D-slice
+// operand holds four column blocks [p3 | p2 | p1 | p0] of BLK columns (C real
+// columns, 1 constant offset column, zero padding); the three int8 MMAs of a
+// K-step write q2 x [p3 p2 p1 p0] at block 0, q1 x [p3 p2 p1] at block 1 and
+// q0 x [p3 p2] at block 2, so accumulator block k collects every product of
+// weight 2^(8 (5 - k)) (q_a p_b with a + b = 5 - k).  4 BLK TMEM columns.
 template <int C, int DA>
 struct Cfg {
     static constexpr int C1 = C + 1;
-    static constexpr int NB = r16(4 * C1), NQ1 = r16(3 * C1), NQ0 = r16(2 * C1);
-    static constexpr int OFF1 = r32(NB), OFF0 = OFF1 + r32(NQ1);
-    static constexpr int ACC_END = OFF0 + r32(NQ0);
+    static_assert(C1 <= 48, "too many columns");
+    static constexpr int BLK = C1 <= 16 ? 16 : (C1 <= 32 ? 32 : 48);
+    static constexpr int NB = 4 * BLK;                         // D-slice rows (MMA N of q2)
+    static constexpr int ACC_END = 4 * BLK;
+    static constexpr int NBUF = (ACC_END + 3 * BK <= 512) ? 3 : 2;   // S/A TMEM buffers
+    static constexpr int STAGES = NBUF + 1;                    // shared-memory ring
     static constexpr int BUF_OFF = ACC_END;                    // NBUF x BK columns
     static constexpr int END = BUF_OFF + NBUF * BK;
     static_assert(END <= 512, "TMEM budget exceeded");
@@ -63,34 +74,28 @@ struct Cfg {
     static constexpr int STAGE_BYTES = B8_BYTES + XB_BYTES;
     static constexpr int AP_BYTES = BM * 3 * DA * 4;           // row operand A' (smem)
     static constexpr int RAW = STAGES * STAGE_BYTES + AP_BYTES + 1024;
+    static_assert(RAW <= 227 * 1024, "shared memory budget exceeded");
     // >= 120 KB so that a single CTA (which owns all 512 TMEM columns) is resident per SM
     static constexpr int SMEM = RAW > 122880 ? RAW : 122880;
 };
 
 // Drain one window's int32 accumulators of this thread's row (TMEM lane)
-// into the fp64 sums acc_sm[c][rl] (c == C: constant offset column).
-// Region a (2, 1, 0 = slices q2 q1 q0) holds column blocks bi = 0..3 of the D
-// slices p3 p2 p1 p0 (weight 2^(8a + 8(3 - bi))), bmax = 4, 3, 2 blocks kept.
-template <int C, int C1>
-__device__ __noinline__ void drain_window(uint32_t lane_base, int nb, int off1, int nq1, int off0,
-                                          int nq0, double (*acc_sm)[BM], int rl) {
-    const int offs[3] = {0, off1, off0}, ns[3] = {nb, nq1, nq0};
+// into the fp64 sums acc_sm[c][rl] (c == C: constant offset column):
+// accumulator block k (BLK columns) carries weight 2^(8 (5 - k)).
+template <int C, int BLK>
+__device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl) {
 #pragma unroll 1
-    for (int reg = 0; reg < 3; reg++) {
-        const int a = 2 - reg, bmax = 4 - reg;
-#pragma unroll 1
-        for (int cb = 0; cb < ns[reg]; cb += 32) {
-            uint32_t r[32];
-            ptx::tmem_ld32(lane_base + offs[reg] + cb, r);
-            ptx::tmem_ld_wait();
+    for (int cb = 0; cb < 4 * BLK; cb += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld32(lane_base + cb, r);
+        ptx::tmem_ld_wait();
 #pragma unroll
-            for (int g = 0; g < 32; g++) {
-                const int col = cb + g;
-                const int bi = col / C1, cc = col - bi * C1;
-                if (bi < bmax) {
-                    const double w = ldexp(1.0, 8 * a + 8 * (3 - bi));
-                    acc_sm[cc][rl] = fma(w, (double)(int32_t)r[g], acc_sm[cc][rl]);
-                }
+        for (int g = 0; g < 32; g++) {
+            const int col = cb + g;
+            const int blk = col / BLK, cc = col - blk * BLK;
+            if (cc <= C) {
+                const double w = ldexp(1.0, 8 * (5 - blk));
+                acc_sm[cc][rl] = fma(w, (double)(int32_t)r[g], acc_sm[cc][rl]);
             }
         }
     }
@@ -108,8 +113,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full_b[STAGES], free_b[STAGES];
-    __shared__ __align__(8) uint64_t s_full[NBUF], a_full[NBUF];
+    __shared__ __align__(8) uint64_t full_b[K::STAGES], free_b[K::STAGES];
+    __shared__ __align__(8) uint64_t s_full[K::NBUF], a_full[K::NBUF];
     __shared__ __align__(8) uint64_t acc_full, acc_empty, init_done;
     __shared__ uint32_t tmem_base_sh;
     __shared__ double acc_sm[C + 1][BM];   // fp64 accumulators (+ constant column)
@@ -121,11 +126,11 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     constexpr int TPW = WINDOW / BK;
 
     if (tid == 0) {
-        for (int q = 0; q < STAGES; q++) {
+        for (int q = 0; q < K::STAGES; q++) {
             ptx::mbar_init(&full_b[q], 1);
             ptx::mbar_init(&free_b[q], 1);
         }
-        for (int q = 0; q < NBUF; q++) {
+        for (int q = 0; q < K::NBUF; q++) {
             ptx::mbar_init(&s_full[q], 1);
             ptx::mbar_init(&a_full[q], 32 * NCW);
         }
@@ -144,8 +149,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // ------------------------------------------------------- producer
         const bool leader = ptx::elect_one();
         for (int t = 0; t < ntl; t++) {
-            const int st = t % STAGES;
-            const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+            const int st = t % K::STAGES;
+            const uint32_t ph = (uint32_t)((t / K::STAGES) & 1);
             if (leader) {
                 ptx::mbar_wait(&free_b[st], ph ^ 1);
                 uint8_t *sb = smem + st * K::STAGE_BYTES;
@@ -160,23 +165,23 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------ MMA issuer
         // One thread issues both MMA kinds.  tcgen05.mma ops of one thread
-        // execute in issue order, so the distance MMA of tile t + NBUF, issued
+        // execute in issue order, so the distance MMA of tile t + K::NBUF, issued
         // right after the int8 MMAs of tile t that read the same TMEM buffer,
         // cannot overwrite it early: no buffer-free round trip is needed.
         constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
-        constexpr uint32_t ID2 = ptx::idesc_i8(BM, K::NB, false, false);
-        constexpr uint32_t ID1 = ptx::idesc_i8(BM, K::NQ1, false, false);
-        constexpr uint32_t ID0 = ptx::idesc_i8(BM, K::NQ0, false, false);
+        constexpr uint32_t ID2 = ptx::idesc_i8(BM, 4 * K::BLK, false, false);
+        constexpr uint32_t ID1 = ptx::idesc_i8(BM, 3 * K::BLK, false, false);
+        constexpr uint32_t ID0 = ptx::idesc_i8(BM, 2 * K::BLK, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         auto issue_dist = [&](int t) {
-            const int st = t % STAGES;
-            const int b = t % NBUF;
-            ptx::mbar_wait(&full_b[st], (uint32_t)((t / STAGES) & 1));
+            const int st = t % K::STAGES;
+            const int b = t % K::NBUF;
+            ptx::mbar_wait(&full_b[st], (uint32_t)((t / K::STAGES) & 1));
             ptx::tc_fence_after();
             if (leader) {
                 const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
-                const uint32_t ap = ptx::smem_u32(smem + STAGES * K::STAGE_BYTES);
+                const uint32_t ap = ptx::smem_u32(smem + K::STAGES * K::STAGE_BYTES);
 #pragma unroll
                 for (int ks = 0; ks < 3 * DA / 8; ks++) {
                     const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
@@ -187,14 +192,14 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             }
             __syncwarp();
         };
-        for (int t = 0; t < NBUF && t < ntl; t++) issue_dist(t);
+        for (int t = 0; t < K::NBUF && t < ntl; t++) issue_dist(t);
         for (int t = 0; t < ntl; t++) {
-            const int st = t % STAGES;
-            const int b = t % NBUF;
+            const int st = t % K::STAGES;
+            const int b = t % K::NBUF;
             const int win = t / TPW;
             const bool first = (t % TPW) == 0;
             if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
-            ptx::mbar_wait(&a_full[b], (uint32_t)((t / NBUF) & 1));
+            ptx::mbar_wait(&a_full[b], (uint32_t)((t / K::NBUF) & 1));
             ptx::tc_fence_after();
             if (leader) {
                 const uint32_t b8 = ptx::smem_u32(smem + st * K::STAGE_BYTES);
@@ -203,15 +208,17 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 for (int ks = 0; ks < BK / 32; ks++) {
                     const uint64_t bd = ptx::smem_desc_kmajor(b8 + ks * 2 * K::NB * 16, K::NB * 16, 128);
                     const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                    ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, ID2, acc);       // q2
-                    ptx::mma_i8_ts(tmem + K::OFF1, aq + 32 * ks + 8, bd, ID1, acc);  // q1
-                    ptx::mma_i8_ts(tmem + K::OFF0, aq + 32 * ks + 0, bd, ID0, acc);  // q0
+                    // q2 spans the whole accumulator: its first MMA of a window
+                    // overwrites; q1 / q0 (issued after it, in order) always add
+                    ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, ID2, acc);             // q2
+                    ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, ID1, 1u);          // q1
+                    ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, ID0, 1u);      // q0
                 }
                 ptx::mma_commit(&free_b[st]);
                 if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
             }
             __syncwarp();
-            if (t + NBUF < ntl) issue_dist(t + NBUF);
+            if (t + K::NBUF < ntl) issue_dist(t + K::NBUF);
         }
     } else {
         // -------------------------------------------------------- compute
@@ -223,7 +230,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32), written to
             // shared memory K-major: [3 DA / 4 chunks][128 rows][4 floats]
             const int rl = sub * 32 + lane;
-            float *ap = reinterpret_cast<float *>(smem + STAGES * K::STAGE_BYTES);
+            float *ap = reinterpret_cast<float *>(smem + K::STAGES * K::STAGE_BYTES);
 #pragma unroll
             for (int q = 0; q < DA; q++) {
                 const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
@@ -246,8 +253,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const uint32_t my_col = lane_base + K::BUF_OFF + JW * h;
         int win = 0;
         for (int t = 0; t < ntl; t++) {
-            const int b = t % NBUF;
-            ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / NBUF) & 1));
+            const int b = t % K::NBUF;
+            ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / K::NBUF) & 1));
             ptx::tc_fence_after();
             uint32_t sv[32];
             const uint32_t col = my_col + b * BK;
@@ -286,8 +293,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             if (last_of_window && h == 0) {
                 ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
                 ptx::tc_fence_after();
-                drain_window<C, K::C1>(lane_base, K::NB, K::OFF1, K::NQ1, K::OFF0, K::NQ0, acc_sm,
-                                       sub * 32 + lane);
+                drain_window<C, K::BLK>(lane_base, acc_sm, sub * 32 + lane);
                 ptx::tc_fence_before();
                 ptx::mbar_arrive_a(a_acce);
                 win++;
@@ -367,7 +373,7 @@ bool k1tc2_supported(int kind, int d, int c) {
     const int da = tc2_da(d);
     switch (c) {
         case 1: case 2: case 4: case 8: case 11: return da <= 24;
-        case 17: return da <= 8;
+        case 17: return da <= 16;
         default: return false;
     }
 }
@@ -458,7 +464,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
     if (nloc > 0) {
         BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
         BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)
-        BBMM_TC2(11, 16) BBMM_TC2(1, 24) BBMM_TC2(2, 24) BBMM_TC2(4, 24)
+        BBMM_TC2(11, 16) BBMM_TC2(17, 16) BBMM_TC2(1, 24) BBMM_TC2(2, 24) BBMM_TC2(4, 24)
         BBMM_TC2(8, 24) BBMM_TC2(11, 24)
         throw Error{BBMM_ERR_ARG, "k1tc2: unsupported (c, d)"};
     }
