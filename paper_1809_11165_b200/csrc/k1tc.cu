@@ -110,9 +110,9 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
 // ======================================================================
 // host side
 // ======================================================================
-// rows of the packed D-slice operand: 4 blocks of BLK >= c + 1 columns
-// (BLK in {16, 32, 48}, matching k1tc2's accumulator blocks)
-int k1tc_bslice_rows(int c) { return 4 * (c + 1 <= 16 ? 16 : (c + 1 <= 32 ? 32 : 48)); }
+// rows of the packed D-slice operand: 4 blocks of BLK = round4(c + 1)
+// columns (matching k1tc2's accumulator blocks)
+int k1tc_bslice_rows(int c) { return 4 * ((c + 1 + 3) & ~3); }
 
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean) {
     tc::k_col_mean<<<d, 256, 0, ctx->stream>>>(X, n, d, mean);

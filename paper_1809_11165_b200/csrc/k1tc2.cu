@@ -42,9 +42,12 @@ namespace tc2 {
 // the MMA side runs two tiles ahead of the slowest warp.
 constexpr int BM = 128, BK = 128;
 constexpr int NQ = BK / 32, JW = BK / NQ, NCW = 4 * NQ;
-// j per TMEM drain: an accumulator column gathers up to 3 slice products of
-// <= 255 x 255 per j, so int32 is safe for < 2^31 / 195075 = 11008 j
-constexpr int WINDOW = 8192;
+// j per TMEM drain.  All slice bytes are unsigned (q2 <= 0x40, p3 <= 0x80),
+// so the accumulators are read as uint32; the largest per-j block sum is
+// block 3: q2 p0 + q1 p1 + q0 p2 <= 64*255 + 2*255*255 = 146370, hence
+// < 2^32 / 146370 = 29343 j per window.
+constexpr int WINDOW = 28672;
+static_assert(WINDOW % BK == 0 && (double)WINDOW * 146370.0 < 4294967296.0, "uint32 window bound");
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(JW == 32, "one 32-column group per warp");
@@ -52,18 +55,22 @@ constexpr __host__ __device__ int r16(int x) { return (x + 15) & ~15; }
 constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
 
 // Accumulator layout: the slice products are merged by weight.  The D-slice
-// operand holds four column blocks [p3 | p2 | p1 | p0] of BLK columns (C real
-// columns, 1 constant offset column, zero padding); the three int8 MMAs of a
-// K-step write q2 x [p3 p2 p1 p0] at block 0, q1 x [p3 p2 p1] at block 1 and
-// q0 x [p3 p2] at block 2, so accumulator block k collects every product of
-// weight 2^(8 (5 - k)) (q_a p_b with a + b = 5 - k).  4 BLK TMEM columns.
+// operand holds four column blocks [p3 | p2 | p1 | p0] of BLK = round4(C + 1)
+// columns (C real columns, 1 constant offset column, zero padding); the three
+// int8 MMAs of a K-step multiply q2, q1, q0 by the whole operand (N = 4 BLK)
+// into accumulator blocks 0-3, 1-4 and 2-5, so block k collects every
+// product of weight 2^(8 (5 - k)) (q_a p_b with a + b = 5 - k): all twelve
+// slice products, no truncation, in 6 BLK TMEM columns.  The MMAs always
+// accumulate; the draining warps zero the columns they read.
 template <int C, int DA>
 struct Cfg {
     static constexpr int C1 = C + 1;
     static_assert(C1 <= 48, "too many columns");
-    static constexpr int BLK = C1 <= 16 ? 16 : (C1 <= 32 ? 32 : 48);
-    static constexpr int NB = 4 * BLK;                         // D-slice rows (MMA N of q2)
-    static constexpr int ACC_END = 4 * BLK;
+    static constexpr int BLK = (C1 + 3) & ~3;
+    static constexpr int NB = 4 * BLK;                         // D-slice rows (MMA N)
+    static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
+    static constexpr int ACC_COLS = 6 * BLK;
+    static constexpr int ACC_END = r32(ACC_COLS);
     static constexpr int NBUF = (ACC_END + 3 * BK <= 512) ? 3 : 2;   // S/A TMEM buffers
     static constexpr int STAGES = NBUF + 1;                    // shared-memory ring
     static constexpr int BUF_OFF = ACC_END;                    // NBUF x BK columns
@@ -81,23 +88,39 @@ struct Cfg {
 
 // Drain one window's int32 accumulators of this thread's row (TMEM lane)
 // into the fp64 sums acc_sm[c][rl] (c == C: constant offset column):
-// accumulator block k (BLK columns) carries weight 2^(8 (5 - k)).
-template <int C, int BLK>
-__device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl) {
-#pragma unroll 1
-    for (int cb = 0; cb < 4 * BLK; cb += 32) {
-        uint32_t r[32];
-        ptx::tmem_ld32(lane_base + cb, r);
-        ptx::tmem_ld_wait();
+// accumulator block k (BLK columns) carries weight 2^(8 (5 - k)).  The four
+// warps of a lane quarter share the work: warp h sums the columns cc with
+// cc % 4 == h (so no two warps touch one acc_sm entry) and zeroes the 32-column
+// chunks q with q % 4 == h for the next window (caller waits for the stores).
+template <int C, int BLK, int ACC_END>
+__device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl, int h) {
+    constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    constexpr int M = (C + 4) / 4;                 // columns cc = h + 4 m <= C per warp
+    uint32_t v[M][6];
 #pragma unroll
-        for (int g = 0; g < 32; g++) {
-            const int col = cb + g;
-            const int blk = col / BLK, cc = col - blk * BLK;
-            if (cc <= C) {
-                const double w = ldexp(1.0, 8 * (5 - blk));
-                acc_sm[cc][rl] = fma(w, (double)(int32_t)r[g], acc_sm[cc][rl]);
-            }
+    for (int m = 0; m < M; m++)
+#pragma unroll
+        for (int k = 0; k < 6; k++)
+            v[m][k] = (h + 4 * m <= C) ? ptx::tmem_ld1(lane_base + k * BLK + h + 4 * m) : 0u;
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const int cc = h + 4 * m;
+        if (cc <= C) {
+            double a = acc_sm[cc][rl];
+#pragma unroll
+            for (int k = 0; k < 6; k++) a = fma(0x1p40 / (double)(1ull << (8 * k)), (double)v[m][k], a);
+            acc_sm[cc][rl] = a;
         }
+    }
+    // every warp has read all columns before any is zeroed: the zeroing
+    // targets only this warp's chunks, read above by all four warps, so
+    // wait for the lane quarter (named barrier over its 4 warps)
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + (rl >> 5)) : "memory");
+#pragma unroll 1
+    for (int q = 32 * h; q < ACC_END; q += 128) {
+#pragma unroll
+        for (int o = 0; o < 32; o += 8) ptx::tmem_st8(lane_base + q + o, z);
     }
 }
 
@@ -135,7 +158,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::mbar_init(&a_full[q], 32 * NCW);
         }
         ptx::mbar_init(&acc_full, 1);
-        ptx::mbar_init(&acc_empty, 128);
+        ptx::mbar_init(&acc_empty, 32 * NCW);
         ptx::mbar_init(&init_done, 128);
         ptx::fence_mbar_init();
     }
@@ -169,11 +192,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // right after the int8 MMAs of tile t that read the same TMEM buffer,
         // cannot overwrite it early: no buffer-free round trip is needed.
         constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
-        constexpr uint32_t ID2 = ptx::idesc_i8(BM, 4 * K::BLK, false, false);
-        constexpr uint32_t ID1 = ptx::idesc_i8(BM, 3 * K::BLK, false, false);
-        constexpr uint32_t ID0 = ptx::idesc_i8(BM, 2 * K::BLK, false, false);
+        constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
+        ptx::tc_fence_after();
         auto issue_dist = [&](int t) {
             const int st = t % K::STAGES;
             const int b = t % K::NBUF;
@@ -207,12 +229,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 #pragma unroll
                 for (int ks = 0; ks < BK / 32; ks++) {
                     const uint64_t bd = ptx::smem_desc_kmajor(b8 + ks * 2 * K::NB * 16, K::NB * 16, 128);
-                    const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                    // q2 spans the whole accumulator: its first MMA of a window
-                    // overwrites; q1 / q0 (issued after it, in order) always add
-                    ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, ID2, acc);             // q2
-                    ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, ID1, 1u);          // q1
-                    ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, ID0, 1u);      // q0
+                    ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, IDQ, 1u);              // q2
+                    ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ, 1u);          // q1
+                    ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ, 1u);      // q0
                 }
                 ptx::mma_commit(&free_b[st]);
                 if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
@@ -243,7 +262,15 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     ap[(k >> 2) * (BM * 4) + rl * 4 + (k & 3)] = parts[pt];
                 }
             }
+            // zero this lane quarter's accumulator columns (the MMAs only add)
+            {
+                constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int q = 0; q < K::ACC_END; q += 8) ptx::tmem_st8(lane_base + q, z);
+                ptx::tmem_st_wait();
+            }
             ptx::fence_proxy_async_smem();
+            ptx::tc_fence_before();
             ptx::mbar_arrive(&init_done);
             for (int c = 0; c <= C; c++) acc_sm[c][rl] = 0.0;
         }
@@ -252,6 +279,49 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const uint32_t a_accf = ptx::smem_u32(&acc_full), a_acce = ptx::smem_u32(&acc_empty);
         const uint32_t my_col = lane_base + K::BUF_OFF + JW * h;
         int win = 0;
+        // Per tile: S = LDTM, A slices = quantise(ex2(S)), STTM over the same
+        // columns, arrive a_full.  The TMEM stores land slowly while the int8
+        // MMAs of the previous tile stream through TMEM, so the arrive for
+        // tile t (and its tcgen05.wait::st) is deferred to the middle of tile
+        // t + 1's MUFU work instead of stalling the warp (K1-TC).
+        auto quant4 = [&](const uint32_t *sv, int u, uint32_t &a0, uint32_t &a1, uint32_t &a2) {
+            uint32_t q[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float sj = __uint_as_float(sv[4 * u + v]);
+                float kv = ex2_approx(sj);
+                // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
+                // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
+                if (MODE == 1) kv *= fmaxf(-1.3862943611198906f * sj, 0.0f);
+                // q = 2 + k~ in [2, 3]: exponent 128 (low bit 0), so the three low
+                // bytes are exactly the 22-bit fixed-point k~ 2^22 (round to nearest)
+                q[v] = __float_as_uint(kv + 2.0f);
+            }
+            const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
+            const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
+            const uint32_t u01 = __byte_perm(q[0], q[1], 0x7351);
+            const uint32_t u23 = __byte_perm(q[2], q[3], 0x7351);
+            a0 = __byte_perm(t01, t23, 0x5410);
+            a2 = __byte_perm(t01, t23, 0x7632);
+            a1 = __byte_perm(u01, u23, 0x5410);
+        };
+        // publish tile tp's A slices (stores issued earlier), then drain the
+        // accumulators if tp closed a window
+        auto publish = [&](int tp) {
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_a(a_afull + 8 * (tp % K::NBUF));
+            const bool last_of_window = ((tp + 1) % TPW) == 0 || tp + 1 == ntl;
+            if (last_of_window) {
+                ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
+                ptx::tc_fence_after();
+                drain_window<C, K::BLK, K::ACC_END>(lane_base, acc_sm, sub * 32 + lane, h);
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive_a(a_acce);
+                win++;
+            }
+        };
         for (int t = 0; t < ntl; t++) {
             const int b = t % K::NBUF;
             ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / K::NBUF) & 1));
@@ -262,43 +332,16 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::tmem_ld_wait();
             uint32_t w0[8], w1[8], w2[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                uint32_t q[4];
+            for (int u = 0; u < 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
+            if (t > 0) publish(t - 1);
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float sj = __uint_as_float(sv[4 * u + v]);
-                    float kv = ex2_approx(sj);
-                    // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
-                    // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
-                    if (MODE == 1) kv *= fmaxf(-1.3862943611198906f * sj, 0.0f);
-                    q[v] = __float_as_uint(fmaf(kv, 0.5f, 1.0f));
-                }
-                const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
-                const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
-                const uint32_t u01 = __byte_perm(q[0], q[1], 0x7351);
-                const uint32_t u23 = __byte_perm(q[2], q[3], 0x7351);
-                w0[u] = __byte_perm(t01, t23, 0x5410);
-                w2[u] = __byte_perm(t01, t23, 0x7632) ^ 0x80808080u;
-                w1[u] = __byte_perm(u01, u23, 0x5410);
-            }
+            for (int u = 4; u < 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
             // overwrite this warp's own S columns with the A slices [q0 | q1 | q2]
             ptx::tmem_st8(col + 0, w0);
             ptx::tmem_st8(col + 8, w1);
             ptx::tmem_st8(col + 16, w2);
-            ptx::tmem_st_wait();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive_a(a_afull + 8 * b);
-
-            const bool last_of_window = ((t + 1) % TPW) == 0 || t + 1 == ntl;
-            if (last_of_window && h == 0) {
-                ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
-                ptx::tc_fence_after();
-                drain_window<C, K::BLK>(lane_base, acc_sm, sub * 32 + lane);
-                ptx::tc_fence_before();
-                ptx::mbar_arrive_a(a_acce);
-                win++;
-            }
         }
+        if (ntl > 0) publish(ntl - 1);
         if (h == 0 && valid) {
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
