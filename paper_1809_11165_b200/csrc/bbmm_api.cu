@@ -161,6 +161,33 @@ __global__ void k_scalar_terms(const double *__restrict__ U, const double *__res
     }
 }
 
+// Outputscale term without a kernel-matmul (reading R25): with
+// Khat = K + sigma^2 I and the mBCG residuals R = B - Khat U (maintained by
+// the recurrence), K U = B - sigma^2 U - R, so by symmetry of K
+//   S_s = sum_a A_a . (K Bd)_a = (1/t) sum_i (K u_i) . Z0_i - u_0 . (K u_0).
+__global__ void k_outputscale_term(const double *__restrict__ U, const double *__restrict__ R,
+                                   const double *__restrict__ B, const double *__restrict__ Z0,
+                                   double noise_var, int64_t nloc, int t, double *__restrict__ part) {
+    const int c = t + 1;
+    const double inv_t = 1.0 / (double)t;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double *u = U + i * c, *r = R + i * c, *b = B + i * c, *z = Z0 + i * c;
+        double s = 0.0;
+        for (int q = 1; q <= t; q++) s += (b[q] - noise_var * u[q] - r[q]) * z[q];
+        acc += s * inv_t - u[0] * (b[0] - noise_var * u[0] - r[0]);
+    }
+    __shared__ double sh[256];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < (int)blockDim.x; q++) s += sh[q];
+        part[blockIdx.x] = s;
+    }
+}
+
 // Derivative-pass operand for the tensor-core path: Bd = [Z0_1..Z0_t / t, -u0] (fp64).
 __global__ void k_build_bd(const double *__restrict__ U, const double *__restrict__ Z0,
                            int64_t nloc, int t, double *__restrict__ Bd) {
@@ -551,8 +578,9 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         double *spart = (double *)ws.get("s_part", (size_t)sblk * 3 * 8);
         const bool tc_deriv = tcop.version == 2 && k1tc2_deriv_supported(h.kind, h.n_ls, d, c);
         if (tc_deriv) {
-            // isotropic RBF: S_l = sum_a A_a . (s K~ o R^2 B)_a, S_s = sum_a A_a . (s K~ B)_a,
-            // two exact tensor-core kernel-matmuls of the packed B = [P^-1 Z / t | -u0]
+            // isotropic RBF: S_l = sum_a A_a . (s K~ o R^2 Bd)_a by one exact tensor-core
+            // kernel-matmul of the packed Bd = [P^-1 Z / t | -u0]; S_s = sum_a A_a . (s K~ Bd)_a
+            // from K U = B - sigma^2 U - R (k_outputscale_term)
             double *Bd = (double *)ws.get("d_Bd", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
             double *Sd = (double *)ws.get("d_S", kMaxCols * 8);
             const int64_t npad_tc = k1tc_pad_rows(rr.nb * ctx->nranks);
@@ -568,13 +596,17 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             const size_t cap = tc_vpart_elems(tcop, n, nloc, c);
             double *Vp = (double *)ws.get("d_Vpart", std::max<size_t>(cap, 1) * 8);
             double *dpart = (double *)ws.get("d_part", (size_t)sblk * 8);
-            for (int mode = 0; mode < 2 && nloc > 0; mode++) {
+            if (nloc > 0) {
+                // S_l at dred[0]: the k~ r^2 kernel-matmul (mode 1)
                 const int sp = tc_matmul(ctx, tcop, Bp, Sd, c, n, rr.r0, nloc, h.s, Vp, cap,
-                                         nullptr, nullptr, mode);
+                                         nullptr, nullptr, 1);
                 k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, (c + 3) & ~3, nloc, t, o.U_d, dpart);
-                ctx->launches++;
-                // mode 1 -> S_l at dred[0]; mode 0 -> S_s at dred[dp]
-                reduce_blocks(ctx, dpart, sblk, 1, dred + (mode == 1 ? 0 : dp));
+                reduce_blocks(ctx, dpart, sblk, 1, dred);
+                // S_s at dred[dp]: from the solves' residual identity (no matmul)
+                k_outputscale_term<<<sblk, 256, 0, sm>>>(o.U_d, o.R_d, B, Z0, h.noise_var, nloc,
+                                                         t, dpart);
+                reduce_blocks(ctx, dpart, sblk, 1, dred + dp);
+                ctx->launches += 2;
             }
             if (nloc > 0) {
                 k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);

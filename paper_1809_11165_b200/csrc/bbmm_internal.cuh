@@ -190,6 +190,7 @@ struct MbcgOut {
     double *Z0 = nullptr;  // optional: initial Phat^{-1} B (nloc x c), may be null
     // device-resident results (workspace; valid until the next library call)
     const double *U_d = nullptr;       // nloc x c solves
+    const double *R_d = nullptr;       // nloc x c recurrence residuals B - Khat U
     const double *ahist_d = nullptr;   // max_iter x c
     const double *bhist_d = nullptr;
     const MbcgState *state_d = nullptr;

@@ -14,12 +14,12 @@
 // Per pair a compute thread then issues ~5 instructions (ex2, 1 FFMA,
 // byte permutes) so the kernel is bound by the MUFU ex2 pipe.
 //
-// CTA = 128 rows, 1 CTA per SM, 18 warps:
-//   warps 0-15: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
-//               h = w / 4 (16 of the 64 j) of every j tile
-//   warp 16   : producer (bulk copies of the B' distance tile and the packed
+// CTA = 128 rows, 1 CTA per SM, 26 warps:
+//   warps 0-23: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
+//               h = w / 4 (16 of the 96 j) of every j tile
+//   warp 24   : producer (bulk copies of the B' distance tile and the packed
 //               D slices)
-//   warp 17   : MMA issuer: int8 contraction of tile t, then the distance
+//   warp 25   : MMA issuer: int8 contraction of tile t, then the distance
 //               MMA of tile t + NBUF into the TMEM buffer just consumed
 #include <algorithm>
 #include <cmath>
@@ -33,24 +33,46 @@
 namespace bbmm {
 namespace tc2 {
 
-// j-tile BK = 128; 16 compute warps, warp (sub, h) serves TMEM lanes
-// 32 sub.. and the j-group h (32 j) of every tile.  Each of the NBUF TMEM
-// buffers (128 columns; NBUF = 3 when the accumulators take <= 128 columns)
-// first receives S (fp32, from the distance MMA); every warp then overwrites
-// ITS OWN 32 S columns with the three int8 slices of its quantised kernel
-// values (24 columns), which the int8 MMAs read as A.  With three buffers
-// the MMA side runs two tiles ahead of the slowest warp.
-constexpr int BM = 128, BK = 128;
-constexpr int NQ = BK / 32, JW = BK / NQ, NCW = 4 * NQ;
+// j-tile BK = 96; 24 compute warps (6 per SM sub-partition, so that one
+// warp's barrier / TMEM latency is covered by the others' MUFU work), warp
+// (sub, h) serves TMEM lanes 32 sub.. and the j-group h (16 j) of every tile.
+// Each of the NBUF TMEM buffers (BK columns; NBUF = 4 when the accumulators
+// take <= 128 columns) first receives S (fp32, from the distance MMA); every
+// warp then overwrites 12 of ITS OWN 16 S columns with the three int8 slices
+// of its quantised kernel values, which the int8 MMAs read as A.  With three
+// buffers the MMA side runs two tiles ahead of the slowest warp.
+//
+// Column maps inside the 32-column group ks = h / 2 of a buffer (eo = h % 2,
+// u, v in 0..3, j' = 16 eo + 4 u + v the point's index within the group):
+//   S  of j'          -> column 8 u + 4 eo + v      (order of the B' rows)
+//   A  slice a, 4 j'  -> column 8 a + 4 eo + u      (K order = j', natural)
+// so the A columns a warp writes (u = 0..2 quarters) are among its own S
+// columns, and each slice's 8 columns hold the 32 j of the group in order.
+#ifndef BBMM_TC2_NPS
+#define BBMM_TC2_NPS 4
+#endif
+#ifndef BBMM_TC2_JW
+#define BBMM_TC2_JW 32
+#endif
+constexpr int NPS = BBMM_TC2_NPS;              // compute warps per lane quarter
+constexpr int JW = BBMM_TC2_JW;                // j per warp per tile (16 or 32)
+constexpr int BM = 128, BK = JW * NPS;         // j tile
+constexpr int NCW = 4 * NPS;
+static_assert((JW == 32 || (JW == 16 && NPS % 2 == 0)) && 32 * (NCW + 2) <= 1024, "CTA shape");
 // j per TMEM drain.  All slice bytes are unsigned (q2 <= 0x40, p3 <= 0x80),
 // so the accumulators are read as uint32; the largest per-j block sum is
 // block 3: q2 p0 + q1 p1 + q0 p2 <= 64*255 + 2*255*255 = 146370, hence
 // < 2^32 / 146370 = 29343 j per window.
-constexpr int WINDOW = 28672;
-static_assert(WINDOW % BK == 0 && (double)WINDOW * 146370.0 < 4294967296.0, "uint32 window bound");
+constexpr int WINDOW = (int)(4294967295ull / 146370ull) / BK * BK;
+static_assert((double)WINDOW * 146370.0 < 4294967296.0, "uint32 window bound");
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
-static_assert(JW == 32, "one 32-column group per warp");
+static_assert(NCW * JW == 4 * BK, "4 lane quarters x BK columns");
+static_assert(BK % 32 == 0, "int8 K-steps of 32");
+// B' row (S column) of point jl in 0..BK-1 of a tile (see the column maps)
+__host__ __device__ constexpr int s_col_of(int jl) {
+    return JW == 32 ? jl : (jl & ~31) + 8 * ((jl >> 2) & 3) + 4 * ((jl >> 4) & 1) + (jl & 3);
+}
 constexpr __host__ __device__ int r16(int x) { return (x + 15) & ~15; }
 constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
 
@@ -71,8 +93,10 @@ struct Cfg {
     static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
     static constexpr int ACC_COLS = 6 * BLK;
     static constexpr int ACC_END = r32(ACC_COLS);
-    static constexpr int NBUF = (ACC_END + 3 * BK <= 512) ? 3 : 2;   // S/A TMEM buffers
-    static constexpr int STAGES = NBUF + 1;                    // shared-memory ring
+    static constexpr int NBUF_FIT = (512 - ACC_END) / BK;
+    static constexpr int NBUF = NBUF_FIT < 4 ? NBUF_FIT : 4;     // S/A TMEM buffers
+    static_assert(NBUF >= 2, "TMEM budget");
+
     static constexpr int BUF_OFF = ACC_END;                    // NBUF x BK columns
     static constexpr int END = BUF_OFF + NBUF * BK;
     static_assert(END <= 512, "TMEM budget exceeded");
@@ -80,32 +104,40 @@ struct Cfg {
     static constexpr int XB_BYTES = 3 * DA * BK * 4;           // tf32 B' per tile
     static constexpr int STAGE_BYTES = B8_BYTES + XB_BYTES;
     static constexpr int AP_BYTES = BM * 3 * DA * 4;           // row operand A' (smem)
+    // Shared-memory ring of NBUF + 1 .. NBUF + 3 stages (as the budget allows):
+    // the issuer checks stage t + NBUF before it waits for tile t's A slices,
+    // i.e. ring depth - NBUF - 1 tile periods after the stage was released.
+    static constexpr int STATIC_BYTES = (C + 1) * BM * 8 + 512;   // acc_sm + barriers
+    static constexpr int STAGES_FIT = (227 * 1024 - STATIC_BYTES - AP_BYTES - 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT < NBUF + 3 ? STAGES_FIT : NBUF + 3;
+    static_assert(STAGES >= NBUF + 1, "shared-memory ring too shallow");
     static constexpr int RAW = STAGES * STAGE_BYTES + AP_BYTES + 1024;
-    static_assert(RAW <= 227 * 1024, "shared memory budget exceeded");
+    static_assert(RAW + STATIC_BYTES <= 227 * 1024, "shared memory budget exceeded");
     // >= 120 KB so that a single CTA (which owns all 512 TMEM columns) is resident per SM
     static constexpr int SMEM = RAW > 122880 ? RAW : 122880;
 };
 
 // Drain one window's int32 accumulators of this thread's row (TMEM lane)
 // into the fp64 sums acc_sm[c][rl] (c == C: constant offset column):
-// accumulator block k (BLK columns) carries weight 2^(8 (5 - k)).  The four
+// accumulator block k (BLK columns) carries weight 2^(8 (5 - k)).  The NPS
 // warps of a lane quarter share the work: warp h sums the columns cc with
-// cc % 4 == h (so no two warps touch one acc_sm entry) and zeroes the 32-column
-// chunks q with q % 4 == h for the next window (caller waits for the stores).
+// cc % NPS == h (so no two warps touch one acc_sm entry) and zeroes the
+// 32-column chunks q with q % NPS == h for the next window (caller waits for
+// the stores).
 template <int C, int BLK, int ACC_END>
 __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl, int h) {
     constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    constexpr int M = (C + 4) / 4;                 // columns cc = h + 4 m <= C per warp
+    constexpr int M = (C + NPS) / NPS;             // columns cc = h + NPS m <= C per warp
     uint32_t v[M][6];
 #pragma unroll
     for (int m = 0; m < M; m++)
 #pragma unroll
         for (int k = 0; k < 6; k++)
-            v[m][k] = (h + 4 * m <= C) ? ptx::tmem_ld1(lane_base + k * BLK + h + 4 * m) : 0u;
+            v[m][k] = (h + NPS * m <= C) ? ptx::tmem_ld1(lane_base + k * BLK + h + NPS * m) : 0u;
     ptx::tmem_ld_wait();
 #pragma unroll
     for (int m = 0; m < M; m++) {
-        const int cc = h + 4 * m;
+        const int cc = h + NPS * m;
         if (cc <= C) {
             double a = acc_sm[cc][rl];
 #pragma unroll
@@ -115,10 +147,10 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[B
     }
     // every warp has read all columns before any is zeroed: the zeroing
     // targets only this warp's chunks, read above by all four warps, so
-    // wait for the lane quarter (named barrier over its 4 warps)
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + (rl >> 5)) : "memory");
+    // wait for the lane quarter (named barrier over its NPS warps)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (rl >> 5)), "n"(32 * NPS) : "memory");
 #pragma unroll 1
-    for (int q = 32 * h; q < ACC_END; q += 128) {
+    for (int q = 32 * h; q < ACC_END; q += 32 * NPS) {
 #pragma unroll
         for (int o = 0; o < 32; o += 8) ptx::tmem_st8(lane_base + q + o, z);
     }
@@ -155,10 +187,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         }
         for (int q = 0; q < K::NBUF; q++) {
             ptx::mbar_init(&s_full[q], 1);
-            ptx::mbar_init(&a_full[q], 32 * NCW);
+            ptx::mbar_init(&a_full[q], NCW);        // one elected lane per warp
         }
         ptx::mbar_init(&acc_full, 1);
-        ptx::mbar_init(&acc_empty, 32 * NCW);
+        ptx::mbar_init(&acc_empty, NCW);
         ptx::mbar_init(&init_done, 128);
         ptx::fence_mbar_init();
     }
@@ -196,10 +228,12 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         ptx::tc_fence_after();
+        auto wait_stage = [&](int t) {
+            ptx::mbar_wait(&full_b[t % K::STAGES], (uint32_t)((t / K::STAGES) & 1));
+        };
         auto issue_dist = [&](int t) {
             const int st = t % K::STAGES;
             const int b = t % K::NBUF;
-            ptx::mbar_wait(&full_b[st], (uint32_t)((t / K::STAGES) & 1));
             ptx::tc_fence_after();
             if (leader) {
                 const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
@@ -214,12 +248,18 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             }
             __syncwarp();
         };
-        for (int t = 0; t < K::NBUF && t < ntl; t++) issue_dist(t);
+        for (int t = 0; t < K::NBUF && t < ntl; t++) {
+            wait_stage(t);
+            issue_dist(t);
+        }
         for (int t = 0; t < ntl; t++) {
             const int st = t % K::STAGES;
             const int b = t % K::NBUF;
             const int win = t / TPW;
             const bool first = (t % TPW) == 0;
+            // operands of the next distance MMA: normally resident long ago, so
+            // this check overlaps the wait for the compute warps below
+            if (t + K::NBUF < ntl) wait_stage(t + K::NBUF);
             if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
             ptx::mbar_wait(&a_full[b], (uint32_t)((t / K::NBUF) & 1));
             ptx::tc_fence_after();
@@ -277,7 +317,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const uint32_t a_sfull = ptx::smem_u32(&s_full[0]);
         const uint32_t a_afull = ptx::smem_u32(&a_full[0]);
         const uint32_t a_accf = ptx::smem_u32(&acc_full), a_acce = ptx::smem_u32(&acc_empty);
-        const uint32_t my_col = lane_base + K::BUF_OFF + JW * h;
+        const uint32_t my_col = lane_base + K::BUF_OFF +
+                                (JW == 32 ? 32 * h : 32 * (h >> 1) + 4 * (h & 1));
         int win = 0;
         // Per tile: S = LDTM, A slices = quantise(ex2(S)), STTM over the same
         // columns, arrive a_full.  The TMEM stores land slowly while the int8
@@ -310,7 +351,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         auto publish = [&](int tp) {
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
-            ptx::mbar_arrive_a(a_afull + 8 * (tp % K::NBUF));
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_a(a_afull + 8 * (tp % K::NBUF));
             const bool last_of_window = ((tp + 1) % TPW) == 0 || tp + 1 == ntl;
             if (last_of_window) {
                 ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
@@ -318,7 +360,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 drain_window<C, K::BLK, K::ACC_END>(lane_base, acc_sm, sub * 32 + lane, h);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive_a(a_acce);
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_a(a_acce);
                 win++;
             }
         };
@@ -326,20 +369,31 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             const int b = t % K::NBUF;
             ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / K::NBUF) & 1));
             ptx::tc_fence_after();
-            uint32_t sv[32];
+            uint32_t sv[JW];
             const uint32_t col = my_col + b * BK;
-            ptx::tmem_ld32(col, sv);
-            ptx::tmem_ld_wait();
-            uint32_t w0[8], w1[8], w2[8];
+            if constexpr (JW == 32) {
+                ptx::tmem_ld32(col, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            } else {
 #pragma unroll
-            for (int u = 0; u < 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
+                for (int u = 0; u < 4; u++) ptx::tmem_ld4(col + 8 * u, sv + 4 * u);
+            }
+            ptx::tmem_ld_wait();
+            uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];
+#pragma unroll
+            for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
             if (t > 0) publish(t - 1);
 #pragma unroll
-            for (int u = 4; u < 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            // overwrite this warp's own S columns with the A slices [q0 | q1 | q2]
-            ptx::tmem_st8(col + 0, w0);
-            ptx::tmem_st8(col + 8, w1);
-            ptx::tmem_st8(col + 16, w2);
+            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
+            // overwrite own S columns with the A slices q0 | q1 | q2 (column maps above)
+            if constexpr (JW == 32) {
+                ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
+                ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
+                ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));
+            } else {
+                ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
+                ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
+                ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
+            }
         }
         if (ntl > 0) publish(ntl - 1);
         if (h == 0 && valid) {
@@ -393,7 +447,7 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
             const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
             const float bl = b - bh;
             const int64_t tt = j / BK;
-            const int jj = (int)(j - tt * BK);
+            const int jj = s_col_of((int)(j - tt * BK));
             float *tile = XB + tt * (int64_t)(3 * DA * BK);
             const float parts[3] = {bh, bl, bh};
             for (int pt = 0; pt < 3; pt++) {

@@ -693,6 +693,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     out.matmul_launches = iters_run;
     out.iters_run = iters_run;
     out.U_d = U;
+    out.R_d = R;
     out.ahist_d = ahist;
     out.bhist_d = bhist;
     out.state_d = st;

@@ -1,6 +1,6 @@
 """Time the C4 full-size kernel-matmul (INT8EXACT) -- variants via env vars."""
 import sys, os, time, numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, '.'); sys.path.insert(0, os.environ.get('BBMM_VARIANT', '.'))
 import synth
 import paper_1809_11165_b200 as bb
 cfg = synth.CONFIGS["C4"]
