@@ -86,44 +86,48 @@ __global__ void k_init_vectors(const double *__restrict__ B, int64_t ldb, int64_
 }
 
 // W partial = L^T R over this block's rows: part[blk][m*c + col].
-// Block = 256 threads (8 warps); a 256-row tile of R is staged in shared
-// memory; for each m every thread forms L[m][row] R[row][:] for its row
-// (coalesced L reads), warps reduce over their 32 rows with shuffles, and the
-// 8 warp partials are added in a fixed order into a per-block k x c
-// accumulator (deterministic).  Grid-stride over row tiles.
+// HBM-bound skinny product (L: k x n fp64 read once).  Block = 8 warps; per
+// chunk of kLtrRows rows the R rows are staged in shared memory, then warp w
+// takes m = w, w + 8, ..: each lane walks rows lane, lane + 32, .. of the
+// chunk (L[m][row] reads coalesced across the warp), keeps the c products in
+// registers, and one shuffle reduction per (m, chunk) adds them into the
+// block's k x c accumulator (each m owned by one warp: deterministic).
 constexpr int kLtrRows = 256;
+template <int CMAX>
 __global__ void __launch_bounds__(256)
 k_LtR(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *__restrict__ R,
       int64_t nloc, int c, double *__restrict__ part) {
     extern __shared__ double sm_ltr[];
     double *Rt = sm_ltr;                          // kLtrRows x c
-    double *wp = Rt + kLtrRows * c;               // 8 warps x c
-    double *acc = wp + 8 * c;                     // k x c block accumulator
+    double *acc = Rt + kLtrRows * c;              // k x c block accumulator
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < k * c; e += 256) acc[e] = 0.0;
     for (int64_t i0 = (int64_t)blockIdx.x * kLtrRows; i0 < nloc;
          i0 += (int64_t)gridDim.x * kLtrRows) {
+        const int rows = (int)(nloc - i0 < kLtrRows ? nloc - i0 : kLtrRows);
         __syncthreads();
-        for (int e = tid; e < kLtrRows * c; e += 256) {
-            const int64_t i = i0 + e / c;
-            Rt[e] = i < nloc ? R[i0 * c + e] : 0.0;
-        }
+        for (int e = tid; e < rows * c; e += 256) Rt[e] = R[i0 * c + e];
         __syncthreads();
-        const int64_t i = i0 + tid;
-        for (int mm = 0; mm < k; mm++) {
-            const double l = i < nloc ? L[(int64_t)mm * n + r0 + i] : 0.0;
-            for (int col = 0; col < c; col++) {
-                double v = l * Rt[tid * c + col];
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) wp[warp * c + col] = v;
+        for (int m = warp; m < k; m += 8) {
+            const double *Lm = L + (int64_t)m * n + r0 + i0;
+            double v[CMAX];
+#pragma unroll
+            for (int q = 0; q < CMAX; q++) v[q] = 0.0;
+            for (int r = lane; r < rows; r += 32) {
+                const double l = Lm[r];
+                const double *rr = Rt + r * c;
+#pragma unroll
+                for (int q = 0; q < CMAX; q++)
+                    if (q < c) v[q] = fma(l, rr[q], v[q]);
             }
-            __syncthreads();
-            for (int col = tid; col < c; col += 256) {
-                double s = 0.0;
-                for (int w = 0; w < 8; w++) s += wp[w * c + col];
-                acc[mm * c + col] += s;
+#pragma unroll
+            for (int q = 0; q < CMAX; q++) {
+                if (q < c) {
+                    double s = v[q];
+                    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    if (lane == 0) acc[m * c + q] += s;
+                }
             }
-            __syncthreads();
         }
     }
     __syncthreads();
@@ -555,14 +559,15 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     // W = L^T R (+ |R|^2 already in red[0..c) when with_rr) -> red[c..c+kc)
     const int ltr_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kLtrRows),
                                                                         2 * kNumSMs));
-    const size_t smem_ltr = ((size_t)kLtrRows * c + 8 * c + (size_t)kk * c) * 8;
+    const size_t smem_ltr = ((size_t)kLtrRows * c + (size_t)kk * c) * 8;
+    auto ltr_kernel = c <= 8 ? k_LtR<8> : (c <= 17 ? k_LtR<17> : (c <= 33 ? k_LtR<33> : k_LtR<kMaxCols>));
     if (smem_ltr > 48 * 1024)
-        BBMM_CUDA(cudaFuncSetAttribute(k_LtR, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BBMM_CUDA(cudaFuncSetAttribute(ltr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_ltr));
     double *part_ltr = (double *)ws.get("cg_part_ltr", (size_t)ltr_blocks * kk * c * 8);
     auto LtR = [&](double *dst) {
         if (k == 0) return;
-        k_LtR<<<ltr_blocks, 256, smem_ltr, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part_ltr);
+        ltr_kernel<<<ltr_blocks, 256, smem_ltr, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part_ltr);
         k_reduce_blocks<<<std::max(1, (int)ceil_div(k * c, 256)), 256, 0, sm>>>(
             part_ltr, ltr_blocks, k * c, dst);
         launches += 2;
