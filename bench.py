@@ -256,9 +256,11 @@ def main():
     achieved = loc_pairs * mufu_per_pair / (mm_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     path = stats[-1]["matmul_path"]
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        if tj.get("kernel_path") == path:     # measured for the kernel timed here
+            traffic = tj.get("dram_bytes_per_launch")
     kname = {0: "k1_onthefly (CUDA-core Khat*D)", 1: "k2_stored (Khat*D)",
              2: "k1tc2_rbf (tcgen05 exact Khat*D)"}[path]
     roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
