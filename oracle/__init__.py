@@ -97,6 +97,8 @@ def _declare(L):
     L.orc_mll_and_grad.argtypes = [_i, _p, _p, _i64, _i, _i, _p, _d, _d, _i, _i, _i, _d, _u64,
                                    _p, _p, _p, _p, _p, _p, _p, _p, _p]
     L.orc_num_threads.restype = _i
+    L.orc_predict.argtypes = [_i, _p, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _i, _i, _d, _p, _p]
+    L.orc_predict.restype = _i
     L.orc_num_threads.argtypes = []
 
 
@@ -334,3 +336,20 @@ def mll_and_grad(kind, X, y, log_ls, log_s, log_noise, t, k, p, tol=0.0, seed=1,
     out = dict(mll=mll.value, grad=grad, U=U, pivots=piv[:k], alpha=al, beta=be, iters=it)
     out.update({kk: stats[i] for i, kk in enumerate(STAT_KEYS)})
     return out
+
+
+# ------------------------------------------------------------ predictions
+def predict(kind, X, y, Xstar, log_ls, log_s, log_noise, k, p, tol=0.0):
+    """Predictive mean and pointwise latent variance, Eq. 1: one mBCG call on
+    [y | k_{X x*}] with the rank-k pivoted-Cholesky preconditioner (the oracle of bbmm_predict)."""
+    X = _f32(X)
+    n, d = X.shape
+    y = _f32(y)
+    Xs = _f32(np.asarray(Xstar).reshape(-1, d))
+    ns = Xs.shape[0]
+    lls = _f64(np.atleast_1d(log_ls))
+    mean, var = np.zeros(ns), np.zeros(ns)
+    _check(lib().orc_predict(kind, _ptr(X), _ptr(y), n, d, _ptr(Xs), ns, lls.size, _ptr(lls),
+                             float(log_s), float(log_noise), k, p, float(tol), _ptr(mean),
+                             _ptr(var)), "predict")
+    return mean, var

@@ -860,6 +860,73 @@ int orc_mll_and_grad(int kind, const float *X32, const float *y32, int64_t n,
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Predictions, Eq. 1 with zero prior mean (R19):                 */
+/*   mean(x*) = k_{X x*}^T Khat^{-1} y                                        */
+/*   var(x*)  = k(x*, x*) - k_{X x*}^T Khat^{-1} k_{X x*}   (pointwise, latent) */
+/* All solves from ONE mBCG call on B = [y | k_{X x*_1} .. k_{X x*_ns}] with  */
+/* the rank-k pivoted-Cholesky preconditioner and no probes (SPEC "predict":   */
+/* "the n* solves performed as one batched mbcg call (probes absent)").       */
+/* ------------------------------------------------------------------------ */
+int orc_predict(int kind, const float *X32, const float *y32, int64_t n, int d,
+                const float *Xs32, int64_t ns, int n_ls, const double *log_ls,
+                double log_s, double log_noise, int k, int p, double tol,
+                double *mean, double *var)
+{
+    hyper_t h;
+    if (n < 1 || ns < 1 || p < 1 || k < 0 || k > n || tol < 0) return ORC_ERR_ARG;
+    double *X = upcast_X(X32, n, d);
+    double *Xs = upcast_X(Xs32, ns, d);
+    int st = hyper_init(&h, kind, X, n, d, n_ls, log_ls, log_s, log_noise);
+    if (st != ORC_OK) { free(X); free(Xs); return st; }
+    const int64_t c = 1 + ns;
+    double *L = (double *)malloc(sizeof(double) * (size_t)n * (k > 0 ? k : 1));
+    int64_t *piv = (int64_t *)malloc(sizeof(int64_t) * (k > 0 ? k : 1));
+    int k_used = 0;
+    double resid = 0.0;
+    /* 1. preconditioner: pivoted Cholesky of K_XX, Woodbury (as for the MLL) */
+    if (k > 0) st = pivchol_kernel(&h, k, L, piv, &k_used, &resid);
+    double *cholC = (double *)malloc(sizeof(double) * (k > 0 ? k * k : 1));
+    double ld_pre = 0.0;
+    const int kp = (k > 0) ? k_used : -1;
+    if (st == ORC_OK) st = orc_precond_setup(L, n, k > 0 ? k : 1, kp, h.noise_var, cholC, &ld_pre);
+    /* 2. B = [y | k_{X x*_q}] */
+    double *B = (double *)malloc(sizeof(double) * (size_t)n * c);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++) {
+        B[i * c] = (double)y32[i];
+        for (int64_t q = 0; q < ns; q++)
+            B[i * c + 1 + q] = orc_kernel(kind, d, X + i * d, Xs + q * d, h.n_ls, h.ls, h.s);
+    }
+    /* 3. one mBCG call */
+    double *U = (double *)malloc(sizeof(double) * (size_t)n * c);
+    double *al = (double *)malloc(sizeof(double) * (size_t)p * c);
+    double *be = (double *)malloc(sizeof(double) * (size_t)p * c);
+    int *it = (int *)malloc(sizeof(int) * c);
+    double *rr = (double *)malloc(sizeof(double) * c);
+    double *rho0 = (double *)malloc(sizeof(double) * c);
+    if (st == ORC_OK) {
+        precond_t P = {L, n, k > 0 ? k : 1, kp, h.noise_var, cholC};
+        st = mbcg_generic(khat_op, &h, &P, n, B, (int)c, p, tol, U, al, be, it, rr, rho0);
+    }
+    /* 4. mean_q = k_q . u_0 ; var_q = k(x*_q, x*_q) - k_q . u_q */
+    if (st == ORC_OK) {
+        for (int64_t q = 0; q < ns; q++) {
+            double m = 0.0, v = 0.0;
+            for (int64_t i = 0; i < n; i++) {
+                m += B[i * c + 1 + q] * U[i * c];
+                v += B[i * c + 1 + q] * U[i * c + 1 + q];
+            }
+            mean[q] = m;
+            if (var)
+                var[q] = orc_kernel(kind, d, Xs + q * d, Xs + q * d, h.n_ls, h.ls, h.s) - v;
+        }
+    }
+    free(X); free(Xs); free(L); free(piv); free(cholC); free(B); free(U); free(al);
+    free(be); free(it); free(rr); free(rho0);
+    return st;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP
