@@ -210,6 +210,26 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X_d,
                                 bbmm_stats_t *stats_h, double *U_d,
                                 int64_t *pivots_h);
 
+/* GP predictions: predictive mean and pointwise latent
+ * variance, Eq. 1, zero prior mean (R19):
+ *   mean[q] = k_{X x*_q}^T Khat^{-1} y
+ *   var[q]  = k(x*_q, x*_q) - k_{X x*_q}^T Khat^{-1} k_{X x*_q}
+ * Every solve is an mBCG solve (bbmm_mbcg semantics, no probes) with the
+ * rank-k pivoted-Cholesky preconditioner, 17 right-hand sides per call
+ * ([y | first 16 test columns], then 17 test columns per call); the kernel
+ * columns k_{X x*} are evaluated in fp64 from X and Xstar.
+ * Inputs (device, fp32, all rows on every rank): X_d n x d, y_d n,
+ *   Xstar_d nstar x d.  0 <= k <= min(n, 128), max_iter >= 1, tol >= 0.
+ * Outputs (device, fp64, nstar each, identical on every rank): mean_d; var_d
+ *   (NULL: mean only -- one solve of y, no solves of test columns).
+ * Errors: BBMM_ERR_ARG (sizes, NULL), BBMM_ERR_DATA (non-finite input),
+ *   BBMM_ERR_NUMERIC (mBCG breakdown). */
+bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X_d, const float *y_d,
+                           int64_t n, int32_t d, const float *Xstar_d,
+                           int64_t nstar, const bbmm_hyper_t *hyper,
+                           bbmm_kmode_t kmode, int32_t k, int32_t max_iter,
+                           double tol, double *mean_d, double *var_d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,9 +82,10 @@ _lib.bbmm_mbcg.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _p, _i32,
                            _p, _i64, _p, _p, _p, _p, _p]
 _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d,
                                    _u64, _p, C.POINTER(_d), _p, C.POINTER(Stats), _p, _p]
+_lib.bbmm_predict.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d, _p, _p]
 for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
            "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
-           "bbmm_mll_and_grad"):
+           "bbmm_mll_and_grad", "bbmm_predict"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -277,3 +278,23 @@ def mll_and_grad(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int
     if U is not None:
         out["U"] = U
     return out
+
+
+def predict(ctx: Context, X, y, Xstar, hyper: Hyper, k: int, max_iter: int = 20, tol: float = 0.0,
+            kmode: int = ONTHEFLY, variance: bool = True):
+    """GP predictive mean and pointwise latent variance, Eq. 1 (bbmm_predict).
+    Returns (mean, var) as fp64 cuda tensors of length nstar (var is None if variance=False)."""
+    torch = _torch()
+    n, d = X.shape
+    ns = Xstar.shape[0]
+    if Xstar.dim() != 2 or Xstar.shape[1] != d:
+        raise ValueError("Xstar must be nstar x d")
+    mean = torch.empty(ns, dtype=torch.float64, device=X.device)
+    var = torch.empty(ns, dtype=torch.float64, device=X.device) if variance else None
+    hp = hyper._c()
+    ctx.check(_lib.bbmm_predict(ctx._h, _dev(X, torch.float32, "X", ctx),
+                                _dev(y, torch.float32, "y", ctx), n, d,
+                                _dev(Xstar, torch.float32, "Xstar", ctx), ns, C.byref(hp), kmode, k,
+                                max_iter, float(tol), _p(mean.data_ptr()),
+                                _p(var.data_ptr()) if var is not None else None))
+    return mean, var

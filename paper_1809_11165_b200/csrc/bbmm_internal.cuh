@@ -202,6 +202,10 @@ struct MbcgOut {
 };
 void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
                    double *cholC, double *logdet_d);
+// predict.cu: mean and pointwise variance (var may be null)
+void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
+                 const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,
+                 int max_iter, double tol, double *mean, double *var);
 void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
               const double *cholC, MbcgOut &out);
 void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, int kgen,

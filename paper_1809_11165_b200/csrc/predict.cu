@@ -1,0 +1,219 @@
+// predict.cu -- SURVEY §8 row f1: GP predictive mean and pointwise latent
+// variance, Eq. 1, zero prior mean (reading R19):
+//   mean(x*) = k_{X x*}^T Khat^{-1} y
+//   var(x*)  = k(x*, x*) - k_{X x*}^T Khat^{-1} k_{X x*}
+// Every solve is an mBCG solve (the same mbcg_run and blackbox matmul as the
+// MLL path) with the rank-k pivoted-Cholesky preconditioner and no probes,
+// batched PRED_COLS right-hand sides at a time: [y | k_{X x*_0..15}] first,
+// then 17 test columns per batch (17 = a tensor-core-supported width; unused
+// columns are zero and freeze at once).  The kernel columns k_{X x*} are
+// evaluated in fp64 from the raw inputs, i.e. the definition, so only the
+// solves carry the blackbox matmul's precision.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "bbmm_internal.cuh"
+
+namespace bbmm {
+
+namespace {
+
+// B[i * ldb + col0 + q] = k(x_{r0+i}, x*_{q0+q}), fp64 (RBF or Matern-5/2)
+__global__ void k_cross_cols(int kind, const float *__restrict__ X, int64_t r0, int64_t nloc,
+                             int d, const float *__restrict__ Xs, int64_t q0, int m,
+                             const double *__restrict__ inv_ls2, double s, double *__restrict__ B,
+                             int ldb, int col0) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / m;
+        const int q = (int)(e - i * m);
+        const float *xi = X + (r0 + i) * d, *xs = Xs + (q0 + q) * d;
+        double r2 = 0.0;
+        for (int a = 0; a < d; a++) {
+            const double df = (double)xi[a] - (double)xs[a];
+            r2 += df * df * inv_ls2[a];
+        }
+        double kv;
+        if (kind == BBMM_RBF) {
+            kv = s * exp(-0.5 * r2);
+        } else {
+            const double r = sqrt(r2), sr = sqrt(5.0) * r;
+            kv = s * (1.0 + sr + (5.0 / 3.0) * r2) * exp(-sr);
+        }
+        B[i * ldb + col0 + q] = kv;
+    }
+}
+
+__global__ void k_y_col(const float *__restrict__ y, int64_t r0, int64_t nloc,
+                        double *__restrict__ B, int ldb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x)
+        B[i * ldb] = (double)y[r0 + i];
+}
+
+__global__ void k_take_col(const double *__restrict__ U, int ldu, int64_t nloc,
+                           double *__restrict__ a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = U[i * ldu];
+}
+
+// Per block: part[blk][q] = sum_i B[i][col0+q] a_i, part[blk][m+q] = sum_i B[i][col0+q] U[i][col0+q]
+// (fixed-order warp then block reduction: deterministic).
+constexpr int kPredMaxM = 17;
+__global__ void __launch_bounds__(256)
+k_pred_dots(const double *__restrict__ B, const double *__restrict__ U, int ld, int col0, int m,
+            const double *__restrict__ a, int64_t nloc, double *__restrict__ part) {
+    double sm_[kPredMaxM], sv_[kPredMaxM];
+#pragma unroll
+    for (int q = 0; q < kPredMaxM; q++) sm_[q] = sv_[q] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double ai = a[i];
+#pragma unroll
+        for (int q = 0; q < kPredMaxM; q++) {
+            if (q < m) {
+                const double b = B[i * ld + col0 + q];
+                sm_[q] = fma(b, ai, sm_[q]);
+                if (U) sv_[q] = fma(b, U[i * ld + col0 + q], sv_[q]);
+            }
+        }
+    }
+    __shared__ double wp[8][2 * kPredMaxM];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kPredMaxM; q++) {
+        double x = sm_[q], y = sv_[q];
+        for (int o = 16; o > 0; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+        }
+        if (lane == 0) { wp[warp][q] = x; wp[warp][kPredMaxM + q] = y; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * m) {
+        const int q = threadIdx.x < m ? threadIdx.x : kPredMaxM + threadIdx.x - m;
+        double acc = 0.0;
+        for (int w = 0; w < 8; w++) acc += wp[w][q];
+        part[(int64_t)blockIdx.x * 2 * m + threadIdx.x] = acc;
+    }
+}
+
+// mean[q0+q] = red[q];  var[q0+q] = s - red[m+q]  (k(x*, x*) = s: stationary kernels)
+__global__ void k_pred_finish(const double *__restrict__ red, int m, double s, int64_t q0,
+                              double *__restrict__ mean, double *__restrict__ var) {
+    const int q = threadIdx.x;
+    if (q < m) {
+        mean[q0 + q] = red[q];
+        if (var) var[q0 + q] = s - red[m + q];
+    }
+}
+
+int pgrid(int64_t work) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 8 * kNumSMs));
+}
+
+}  // namespace
+
+void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
+                 const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,
+                 int max_iter, double tol, double *mean, double *var) {
+    cudaStream_t sm = ctx->stream;
+    Workspace &ws = ctx->ws;
+    constexpr int CW = kPredMaxM;                  // right-hand sides per mBCG call
+    const RowRange rr = local_rows(ctx, n);
+    const int64_t nloc = rr.count();
+    const int dp = pad_dim(d), ds = (dp + 3) & ~3;
+    float *Xs = (float *)ws.get("Xs", (size_t)n * ds * 4);
+    scale_inputs(ctx, X, n, d, h, Xs, dp);
+
+    // preconditioner (as for the MLL: pivoted Cholesky of K_XX, Woodbury)
+    double *L = (double *)ws.get("L", (size_t)std::max(k, 1) * n * 8);
+    int k_used = 0;
+    double resid = 0.0;
+    std::vector<int64_t> piv(std::max(k, 1), -1);
+    if (k > 0) pivchol(ctx, X, n, d, h, k, L, piv.data(), &k_used, &resid);
+    double *cholC = (double *)ws.get("cholC", (size_t)std::max(k, 1) * std::max(k, 1) * 8);
+    double *ldp = (double *)ws.get("logdet_pre", 8);
+    precond_setup(ctx, L, n, k > 0 ? k_used : 0, h.noise_var, cholC, ldp);
+    float *Kst = nullptr;
+    if (stored && nloc > 0) {
+        const int64_t ldk = ((n + 3) / 4) * 4;
+        Kst = (float *)ws.get("Kst", (size_t)nloc * ldk * 4);
+        build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
+    }
+    TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, CW, h, rr.nb * ctx->nranks);
+    MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
+               k > 0 ? k_used : 0, CW, max_iter, tol};
+
+    double inv_ls2[kMaxDim];
+    for (int q = 0; q < d; q++) {
+        const double l = h.ls[h.n_ls == 1 ? 0 : q];
+        inv_ls2[q] = 1.0 / (l * l);
+    }
+    double *inv_d = (double *)ws.get("pred_inv_ls2", sizeof(inv_ls2));
+    BBMM_CUDA(cudaMemcpyAsync(inv_d, inv_ls2, sizeof(double) * d, cudaMemcpyHostToDevice, sm));
+    const int64_t nl1 = std::max<int64_t>(nloc, 1);
+    double *B = (double *)ws.get("pred_B", (size_t)nl1 * CW * 8);
+    double *alpha = (double *)ws.get("pred_alpha", (size_t)nl1 * 8);
+    const int nblk = pgrid(nl1);
+    double *part = (double *)ws.get("pred_part", (size_t)nblk * 2 * CW * 8);
+    double *red = (double *)ws.get("pred_red", 2 * CW * 8);
+    auto cross = [&](int64_t q0, int m, int col0) {
+        if (nloc > 0 && m > 0) {
+            k_cross_cols<<<pgrid(nloc * m), 256, 0, sm>>>(h.kind, X, rr.r0, nloc, d, Xstar, q0,
+                                                            m, inv_d, h.s, B, CW, col0);
+            ctx->launches++;
+        }
+    };
+    auto dots = [&](const double *U, int col0, int m, int64_t q0) {
+        if (nloc > 0) {
+            k_pred_dots<<<nblk, 256, 0, sm>>>(B, U, CW, col0, m, alpha, nloc, part);
+            ctx->launches++;
+            reduce_blocks(ctx, part, nblk, 2 * m, red);
+        } else {
+            BBMM_CUDA(cudaMemsetAsync(red, 0, 2 * m * 8, sm));
+        }
+        allreduce_sum(ctx, red, (size_t)2 * m);
+        k_pred_finish<<<1, 32, 0, sm>>>(red, m, h.s, q0, mean, U ? var : nullptr);
+        ctx->launches++;
+    };
+
+    // batch 0: [y | first test columns] (variance) or [y] alone (mean only)
+    BBMM_CUDA(cudaMemsetAsync(B, 0, (size_t)nl1 * CW * 8, sm));
+    if (nloc > 0) {
+        k_y_col<<<pgrid(nloc), 256, 0, sm>>>(y, rr.r0, nloc, B, CW);
+        ctx->launches++;
+    }
+    const int m0 = var ? (int)std::min<int64_t>(nstar, CW - 1) : 0;
+    cross(0, m0, 1);
+    MbcgOut o;
+    mbcg_run(ctx, a, B, CW, cholC, o);
+    if (nloc > 0) {
+        k_take_col<<<pgrid(nloc), 256, 0, sm>>>(o.U_d, CW, nloc, alpha);
+        ctx->launches++;
+    }
+    if (var) {
+        if (m0 > 0) dots(o.U_d, 1, m0, 0);
+        // later batches: CW test columns each, solved together
+        for (int64_t q0 = m0; q0 < nstar; q0 += CW) {
+            const int m = (int)std::min<int64_t>(nstar - q0, CW);
+            BBMM_CUDA(cudaMemsetAsync(B, 0, (size_t)nl1 * CW * 8, sm));
+            cross(q0, m, 0);
+            MbcgOut ob;
+            mbcg_run(ctx, a, B, CW, cholC, ob);
+            dots(ob.U_d, 0, m, q0);
+        }
+    } else {
+        // mean only: k_{X x*}^T alpha, no further solves
+        for (int64_t q0 = 0; q0 < nstar; q0 += CW) {
+            const int m = (int)std::min<int64_t>(nstar - q0, CW);
+            cross(q0, m, 0);
+            dots(nullptr, 0, m, q0);
+        }
+    }
+    BBMM_LAUNCH_CHECK();
+}
+
+}  // namespace bbmm

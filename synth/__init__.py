@@ -109,6 +109,13 @@ def make_problem(cfg: Config, seed: int = 0) -> Problem:
     return Problem(cfg, X, y, log_ls, math.log(cfg.outputscale), 0.5 * math.log(cfg.noise_var))
 
 
+def test_points(cfg: Config, ns: int, seed: int = 7) -> np.ndarray:
+    """ns x d float32 test inputs x* from the same distribution as X (predictions, row f1)."""
+    rng = np.random.default_rng(seed)
+    Xs = rng.random((ns, cfg.d)) if cfg.x_dist == "uniform01" else rng.standard_normal((ns, cfg.d))
+    return Xs.astype(np.float32)
+
+
 def random_block(n: int, c: int, seed: int) -> np.ndarray:
     """A dense n x c float32 block [N(0,1) | Rademacher] used as a matmul RHS."""
     rng = np.random.default_rng(seed)
