@@ -99,6 +99,9 @@ def _declare(L):
     L.orc_num_threads.restype = _i
     L.orc_predict.argtypes = [_i, _p, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _i, _i, _d, _p, _p]
     L.orc_predict.restype = _i
+    L.orc_train_adam.argtypes = [_i, _p, _p, _i64, _i, _i, _p, _i, _i, _i, _d, _u64, _i, _d, _d,
+                                 _d, _d, _p, _p]
+    L.orc_train_adam.restype = _i
     L.orc_num_threads.argtypes = []
 
 
@@ -353,3 +356,21 @@ def predict(kind, X, y, Xstar, log_ls, log_s, log_noise, k, p, tol=0.0):
                              float(log_s), float(log_noise), k, p, float(tol), _ptr(mean),
                              _ptr(var)), "predict")
     return mean, var
+
+
+# ------------------------------------------------------------ training
+def train_adam(kind, X, y, log_ls, log_s, log_noise, t, k, p, steps, lr=0.1, b1=0.9, b2=0.999,
+               eps=1e-8, tol=0.0, seed=1):
+    """Adam on theta = (log l.., log s, log sigma) with the BBMM gradient (reading R26).
+    Returns (theta_final, trace) with trace rows [mll(theta_s), theta_s...]."""
+    X = _f32(X)
+    n, d = X.shape
+    y = _f32(y)
+    th0 = _f64(np.concatenate([np.atleast_1d(log_ls), [log_s, log_noise]]))
+    nls = th0.size - 2
+    out = np.zeros_like(th0)
+    trace = np.zeros((max(steps, 1), 1 + th0.size))
+    _check(lib().orc_train_adam(kind, _ptr(X), _ptr(y), n, d, nls, _ptr(th0), t, k, p, float(tol),
+                                int(seed) & (2**64 - 1), steps, float(lr), float(b1), float(b2),
+                                float(eps), _ptr(out), _ptr(trace)), "train_adam")
+    return out, trace[:steps]

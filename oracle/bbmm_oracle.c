@@ -927,6 +927,53 @@ int orc_predict(int kind, const float *X32, const float *y32, int64_t n, int d,
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Hyperparameter training ("All methods use the same optimizer        */
+/* (Adam)"; settings unstated -> reading R26): `steps` Adam steps (Kingma &  */
+/* Ba) on theta = (log l.., log s, log sigma) minimising -mll with the BBMM  */
+/* gradient of orc_mll_and_grad, fresh probes each step (seed + step):       */
+/*   g = -grad ; m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2                 */
+/*   theta -= lr (m / (1 - b1^s)) / (sqrt(v / (1 - b2^s)) + eps)              */
+/* trace (steps x (1 + ntheta), may be NULL): row s = [mll(theta_s), theta_s]. */
+/* ------------------------------------------------------------------------ */
+int orc_train_adam(int kind, const float *X32, const float *y32, int64_t n, int d,
+                   int n_ls, const double *theta0, int t, int k, int p, double tol,
+                   uint64_t seed, int steps, double lr, double b1, double b2,
+                   double eps, double *theta_out, double *trace)
+{
+    const int nt = n_ls + 2;
+    if (steps < 0 || !(lr > 0) || b1 < 0 || b1 >= 1 || b2 < 0 || b2 >= 1 || eps < 0)
+        return ORC_ERR_ARG;
+    double *th = (double *)malloc(sizeof(double) * nt);
+    double *g = (double *)malloc(sizeof(double) * nt);
+    double *m1 = (double *)calloc(nt, sizeof(double));
+    double *m2 = (double *)calloc(nt, sizeof(double));
+    memcpy(th, theta0, sizeof(double) * nt);
+    int st = ORC_OK;
+    for (int s = 0; s < steps && st == ORC_OK; s++) {
+        double mll = 0.0;
+        st = orc_mll_and_grad(kind, X32, y32, n, d, n_ls, th, th[n_ls], th[n_ls + 1], t, k, p,
+                              tol, seed + (uint64_t)s, NULL, &mll, g, NULL, NULL, NULL, NULL,
+                              NULL, NULL);
+        if (st != ORC_OK) break;
+        if (!isfinite(mll)) { st = ORC_ERR_NUMERIC; break; }
+        if (trace) {
+            trace[(int64_t)s * (1 + nt)] = mll;
+            memcpy(trace + (int64_t)s * (1 + nt) + 1, th, sizeof(double) * nt);
+        }
+        const double c1 = 1.0 - pow(b1, s + 1), c2 = 1.0 - pow(b2, s + 1);
+        for (int q = 0; q < nt; q++) {
+            const double gq = -g[q];                   /* minimise -mll */
+            m1[q] = b1 * m1[q] + (1.0 - b1) * gq;
+            m2[q] = b2 * m2[q] + (1.0 - b2) * gq * gq;
+            th[q] -= lr * (m1[q] / c1) / (sqrt(m2[q] / c2) + eps);
+        }
+    }
+    memcpy(theta_out, th, sizeof(double) * nt);
+    free(th); free(g); free(m1); free(m2);
+    return st;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP
