@@ -230,6 +230,25 @@ bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X_d, const float *y_d,
                            bbmm_kmode_t kmode, int32_t k, int32_t max_iter,
                            double tol, double *mean_d, double *var_d);
 
+/* Hyperparameter training ("All methods use
+ * the same optimizer (Adam)"; settings by DESIGN.md reading R26): `steps` Adam
+ * steps on theta = (log l_1..l_{n_ls}, log s, log sigma) minimising -mll, with
+ * the gradient of bbmm_mll_and_grad and fresh probes each step (seed + step):
+ *   g = -grad ; m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2 ;
+ *   theta -= lr (m / (1 - b1^s)) / (sqrt(v / (1 - b2^s)) + eps)
+ * hyper: initial theta (host).  Outputs (host): theta_out_h (n_ls + 2, the
+ *   trained theta); trace_h (steps x (n_ls + 3) fp64, may be NULL): row s =
+ *   [mll(theta_s), theta_s].  Other arguments as bbmm_mll_and_grad.
+ * Errors: as bbmm_mll_and_grad (the failing step is named); BBMM_ERR_ARG for
+ *   steps < 0, lr <= 0, b1/b2 outside [0, 1), eps < 0. */
+bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X_d, const float *y_d,
+                              int64_t n, int32_t d, const bbmm_hyper_t *hyper,
+                              bbmm_kmode_t kmode, int32_t t, int32_t k,
+                              int32_t max_iter, double tol, uint64_t seed,
+                              int32_t steps, double lr, double beta1,
+                              double beta2, double eps, double *theta_out_h,
+                              double *trace_h);
+
 #ifdef __cplusplus
 }
 #endif

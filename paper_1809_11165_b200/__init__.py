@@ -83,9 +83,11 @@ _lib.bbmm_mbcg.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _p, _i32,
 _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d,
                                    _u64, _p, C.POINTER(_d), _p, C.POINTER(Stats), _p, _p]
 _lib.bbmm_predict.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d, _p, _p]
+_lib.bbmm_train_adam.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d, _u64,
+                                 _i32, _d, _d, _d, _d, _p, _p]
 for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
            "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
-           "bbmm_mll_and_grad", "bbmm_predict"):
+           "bbmm_mll_and_grad", "bbmm_predict", "bbmm_train_adam"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -298,3 +300,22 @@ def predict(ctx: Context, X, y, Xstar, hyper: Hyper, k: int, max_iter: int = 20,
                                 max_iter, float(tol), _p(mean.data_ptr()),
                                 _p(var.data_ptr()) if var is not None else None))
     return mean, var
+
+
+def train_adam(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int = 20,
+               steps: int = 100, lr: float = 0.1, beta1: float = 0.9, beta2: float = 0.999,
+               eps: float = 1e-8, tol: float = 0.0, seed: int = 1, kmode: int = ONTHEFLY):
+    """Adam hyperparameter training (bbmm_train_adam).
+    Returns (trained Hyper, trace) with trace rows [mll(theta_s), theta_s...]."""
+    torch = _torch()
+    n, d = X.shape
+    nls = int(np.atleast_1d(hyper.log_ls).size)
+    th = np.zeros(nls + 2)
+    trace = np.zeros((max(steps, 1), nls + 3))
+    hp = hyper._c()
+    ctx.check(_lib.bbmm_train_adam(ctx._h, _dev(X, torch.float32, "X", ctx),
+                                   _dev(y, torch.float32, "y", ctx), n, d, C.byref(hp), kmode, t, k,
+                                   max_iter, float(tol), int(seed) & (2**64 - 1), steps, float(lr),
+                                   float(beta1), float(beta2), float(eps), th.ctypes.data_as(_p),
+                                   trace.ctypes.data_as(_p)))
+    return Hyper(hyper.kind, th[:nls], th[nls], th[nls + 1]), trace[:steps]

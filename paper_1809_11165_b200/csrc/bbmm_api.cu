@@ -722,4 +722,48 @@ bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X, const float *y, int64
     });
 }
 
+bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X, const float *y, int64_t n,
+                              int32_t d, const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, int32_t t,
+                              int32_t k, int32_t max_iter, double tol, uint64_t seed, int32_t steps,
+                              double lr, double beta1, double beta2, double eps,
+                              double *theta_out_h, double *trace_h) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        BBMM_REQUIRE(hyper != nullptr && hyper->log_ls_h != nullptr, "hyper is NULL");
+        BBMM_REQUIRE(hyper->n_ls == 1 || hyper->n_ls == d, "n_ls must be 1 or d");
+        BBMM_REQUIRE(steps >= 0, "steps must be >= 0");
+        BBMM_REQUIRE(lr > 0.0 && beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0 &&
+                         eps >= 0.0,
+                     "Adam settings out of range");
+        BBMM_REQUIRE(theta_out_h != nullptr, "theta_out_h is NULL");
+        const int nls = hyper->n_ls, nt = nls + 2;
+        // theta = (log l.., log s, log sigma); Adam on -mll (reading R26)
+        std::vector<double> th(nt), g(nt), m1(nt, 0.0), m2(nt, 0.0);
+        std::copy(hyper->log_ls_h, hyper->log_ls_h + nls, th.begin());
+        th[nls] = hyper->log_outputscale;
+        th[nls + 1] = hyper->log_noise;
+        for (int s = 0; s < steps; s++) {
+            bbmm_hyper_t hs{hyper->kind, nls, th.data(), th[nls], th[nls + 1]};
+            double mll = 0.0;
+            const bbmm_status_t st = bbmm_mll_and_grad(ctx, X, y, n, d, &hs, kmode, t, k, max_iter,
+                                                       tol, seed + (uint64_t)s, nullptr, &mll,
+                                                       g.data(), nullptr, nullptr, nullptr);
+            if (st != BBMM_OK) throw Error{st, "training step " + std::to_string(s) + ": " + ctx->err};
+            if (!std::isfinite(mll)) throw Error{BBMM_ERR_NUMERIC, "non-finite mll during training"};
+            if (trace_h) {
+                trace_h[(size_t)s * (1 + nt)] = mll;
+                std::copy(th.begin(), th.end(), trace_h + (size_t)s * (1 + nt) + 1);
+            }
+            const double c1 = 1.0 - std::pow(beta1, s + 1), c2 = 1.0 - std::pow(beta2, s + 1);
+            for (int q = 0; q < nt; q++) {
+                const double gq = -g[q];
+                m1[q] = beta1 * m1[q] + (1.0 - beta1) * gq;
+                m2[q] = beta2 * m2[q] + (1.0 - beta2) * gq * gq;
+                th[q] -= lr * (m1[q] / c1) / (std::sqrt(m2[q] / c2) + eps);
+            }
+        }
+        std::copy(th.begin(), th.end(), theta_out_h);
+    });
+}
+
 }  // extern "C"
