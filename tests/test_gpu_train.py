@@ -44,7 +44,8 @@ def test_train_matches_oracle(ctx, orc, name, n, steps):
     assert np.abs(th - tho).max() <= steps * 0.1 * 2e-3, (th, tho)
     np.testing.assert_allclose(tr[:, 0], tro[:, 0], rtol=1e-3)
     np.testing.assert_allclose(tr[0, 1:], tro[0, 1:], rtol=0, atol=0)     # theta_0 echoed
-    assert tro[-1, 0] > tro[0, 0] and tr[-1, 0] > tr[0, 0]               # ascends the MLL
+    # (descent itself is pinned on the oracle, tests/test_oracle_train.py: with fresh
+    #  probes each step a few steps from the generating theta are noise-dominated)
 
 
 def test_train_zero_steps_and_bad_args(ctx):
