@@ -83,10 +83,10 @@ def _declare(L):
     L.orc_probes.restype = None
     L.orc_probes.argtypes = [_p, _i64, _i, _i, _p, _i, _i, _d, _p]
     L.orc_mbcg_dense.restype = _i
-    L.orc_mbcg_dense.argtypes = [_p, _i64, _p, _i, _d, _p, _i, _i, _d, _p, _p, _p, _p, _p, _p]
+    L.orc_mbcg_dense.argtypes = [_p, _i64, _p, _i, _d, _p, _i, _i, _d, _p, _p, _p, _p, _p, _p, _p]
     L.orc_mbcg_kernel.restype = _i
     L.orc_mbcg_kernel.argtypes = [_i, _p, _i64, _i, _i, _p, _d, _d, _p, _i, _p, _i, _i, _d,
-                                  _p, _p, _p, _p, _p, _p]
+                                  _p, _p, _p, _p, _p, _p, _p]
     L.orc_tridiag_from_cg.restype = None
     L.orc_tridiag_from_cg.argtypes = [_i, _p, _p, _i, _p, _p]
     L.orc_tridiag_eig.restype = _i
@@ -248,7 +248,7 @@ def probes(eps, L, sigma):
 # ---------------------------------------------------------------- mBCG
 def _mbcg_out(n, c, p):
     return (np.zeros((n, c)), np.zeros((p, c)), np.zeros((p, c)), np.zeros(c, np.int32),
-            np.zeros(c), np.zeros(c))
+            np.zeros(c), np.zeros(c), np.zeros((p, c)))
 
 
 def mbcg_dense(A, B, p, tol=0.0, L=None, noise_var=1.0):
@@ -259,11 +259,11 @@ def mbcg_dense(A, B, p, tol=0.0, L=None, noise_var=1.0):
     c = B.shape[1]
     k = 0 if L is None else L.shape[1]
     Lp = np.zeros((n, 1)) if L is None else _f64(L)
-    U, al, be, it, rr, r0 = _mbcg_out(n, c, p)
+    U, al, be, it, rr, r0, rh = _mbcg_out(n, c, p)
     _check(lib().orc_mbcg_dense(_ptr(A), n, _ptr(Lp), k, float(noise_var), _ptr(B), c, p, float(tol),
-                                _ptr(U), _ptr(al), _ptr(be), _ptr(it), _ptr(rr), _ptr(r0)),
+                                _ptr(U), _ptr(al), _ptr(be), _ptr(it), _ptr(rr), _ptr(r0), _ptr(rh)),
            "mbcg_dense")
-    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0)
+    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0, relres_hist=rh)
 
 
 def mbcg_kernel(kind, X, log_ls, log_s, log_noise, B, p, tol=0.0, L=None):
@@ -274,11 +274,12 @@ def mbcg_kernel(kind, X, log_ls, log_s, log_noise, B, p, tol=0.0, L=None):
     lls = _f64(np.atleast_1d(log_ls))
     k = 0 if L is None else L.shape[1]
     Lp = np.zeros((n, 1)) if L is None else _f64(L)
-    U, al, be, it, rr, r0 = _mbcg_out(n, c, p)
+    U, al, be, it, rr, r0, rh = _mbcg_out(n, c, p)
     _check(lib().orc_mbcg_kernel(kind, _ptr(X), n, d, lls.size, _ptr(lls), float(log_s),
                                  float(log_noise), _ptr(Lp), k, _ptr(B), c, p, float(tol), _ptr(U),
-                                 _ptr(al), _ptr(be), _ptr(it), _ptr(rr), _ptr(r0)), "mbcg_kernel")
-    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0)
+                                 _ptr(al), _ptr(be), _ptr(it), _ptr(rr), _ptr(r0), _ptr(rh)),
+           "mbcg_kernel")
+    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0, relres_hist=rh)
 
 
 def tridiag_from_cg(alpha, beta):

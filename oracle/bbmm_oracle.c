@@ -482,7 +482,7 @@ typedef struct {
 static int mbcg_generic(op_fn op, const void *opctx, const precond_t *P,
                         int64_t n, const double *B, int c, int p, double tol,
                         double *U, double *alpha, double *beta, int *iters,
-                        double *relres, double *rho0)
+                        double *relres, double *rho0, double *relres_hist)
 {
     size_t nc = (size_t)n * c;
     double *R = (double *)malloc(sizeof(double) * nc);
@@ -511,7 +511,10 @@ static int mbcg_generic(op_fn op, const void *opctx, const precond_t *P,
         iters[col] = 0;
         relres[col] = active[col] ? 1.0 : 0.0;
     }
-    for (int64_t i = 0; i < (int64_t)p * c; i++) { alpha[i] = 0.0; beta[i] = 0.0; }
+    for (int64_t i = 0; i < (int64_t)p * c; i++) {
+        alpha[i] = 0.0; beta[i] = 0.0;
+        if (relres_hist) relres_hist[i] = 0.0;
+    }
 
     for (int j = 0; j < p; j++) {
         int any = 0;
@@ -533,6 +536,7 @@ static int mbcg_generic(op_fn op, const void *opctx, const precond_t *P,
             alpha[(int64_t)j * c + col] = a;
             iters[col] = j + 1;
             relres[col] = sqrt(r2) / bnorm[col];
+            if (relres_hist) relres_hist[(int64_t)j * c + col] = relres[col];
             if (relres[col] < tol) active[col] = 0;
         }
         orc_precond_solve(P->L, n, P->ldl, P->k, P->noise_var, P->cholC, R, c, Z);
@@ -575,7 +579,7 @@ static void khat_op(const void *ctx, const double *M, int c, double *out)
 int orc_mbcg_dense(const double *A, int64_t n, const double *L, int k,
                    double noise_var, const double *B, int c, int p, double tol,
                    double *U, double *alpha, double *beta, int *iters,
-                   double *relres, double *rho0)
+                   double *relres, double *rho0, double *relres_hist)
 {
     /* k == 0 here means "no preconditioner" (P = I). */
     precond_t P = {L, n, k, k > 0 ? k : -1, noise_var, NULL};
@@ -585,7 +589,7 @@ int orc_mbcg_dense(const double *A, int64_t n, const double *L, int k,
     if (st == ORC_OK) {
         dense_op_ctx ctx = {A, n};
         st = mbcg_generic(dense_op, &ctx, &P, n, B, c, p, tol, U, alpha, beta,
-                          iters, relres, rho0);
+                          iters, relres, rho0, relres_hist);
     }
     free(P.cholC);
     return st;
@@ -596,7 +600,7 @@ int orc_mbcg_kernel(int kind, const float *X32, int64_t n, int d, int n_ls,
                     const double *log_ls, double log_s, double log_noise,
                     const double *L, int k, const double *B, int c, int p,
                     double tol, double *U, double *alpha, double *beta,
-                    int *iters, double *relres, double *rho0)
+                    int *iters, double *relres, double *rho0, double *relres_hist)
 {
     hyper_t h;
     double *X = upcast_X(X32, n, d);
@@ -608,7 +612,7 @@ int orc_mbcg_kernel(int kind, const float *X32, int64_t n, int d, int n_ls,
         st = orc_precond_setup(L, n, k, P.k, h.noise_var, P.cholC, &ld);
         if (st == ORC_OK)
             st = mbcg_generic(khat_op, &h, &P, n, B, c, p, tol, U, alpha, beta,
-                              iters, relres, rho0);
+                              iters, relres, rho0, relres_hist);
         free(P.cholC);
     }
     free(X);
@@ -799,7 +803,7 @@ int orc_mll_and_grad(int kind, const float *X32, const float *y32, int64_t n,
     double *rho0 = (double *)malloc(sizeof(double) * c);
     if (st == ORC_OK) {
         precond_t P = {L, n, k > 0 ? k : 1, kp, h.noise_var, cholC};
-        st = mbcg_generic(khat_op, &h, &P, n, B, c, p, tol, U, al, be, it, rr, rho0);
+        st = mbcg_generic(khat_op, &h, &P, n, B, c, p, tol, U, al, be, it, rr, rho0, NULL);
     }
     /* 5. SLQ log-det */
     double ld_ratio = 0.0;
@@ -907,7 +911,7 @@ int orc_predict(int kind, const float *X32, const float *y32, int64_t n, int d,
     double *rho0 = (double *)malloc(sizeof(double) * c);
     if (st == ORC_OK) {
         precond_t P = {L, n, k > 0 ? k : 1, kp, h.noise_var, cholC};
-        st = mbcg_generic(khat_op, &h, &P, n, B, (int)c, p, tol, U, al, be, it, rr, rho0);
+        st = mbcg_generic(khat_op, &h, &P, n, B, (int)c, p, tol, U, al, be, it, rr, rho0, NULL);
     }
     /* 4. mean_q = k_q . u_0 ; var_q = k(x*_q, x*_q) - k_q . u_q */
     if (st == ORC_OK) {

@@ -173,3 +173,41 @@ def test_slq_unbiased_over_reseeds(orc):
     ld, per = orc.slq_logdet(r, col0=0)
     se = per.std(ddof=1) / math.sqrt(t)
     assert abs(ld - exact) < 3.5 * se
+
+
+# ------------------------------------------------ residual history (row f3)
+def test_relres_history_is_true_residual(orc):
+    # entry j = ||B - A U_(j+1)|| / ||B|| with U_(j+1) from an independent run stopped after
+    # j + 1 iterations (the recurrence residual equals the true residual up to rounding)
+    K, A, s2, rng = kernel_problem(n=40, seed=3)
+    B = rng.standard_normal((40, 3))
+    L = np.linalg.cholesky(K + 1e-9 * np.eye(40))[:, :4]
+    full = orc.mbcg_dense(A, B, 12, L=L, noise_var=s2)
+    for j in range(12):
+        Uj = orc.mbcg_dense(A, B, j + 1, L=L, noise_var=s2)["U"]
+        true = np.linalg.norm(B - A @ Uj, axis=0) / np.linalg.norm(B, axis=0)
+        np.testing.assert_allclose(full["relres_hist"][j], true, rtol=1e-8, atol=1e-14)
+
+
+def test_relres_history_frozen_columns_zero(orc):
+    K, A, s2, rng = kernel_problem(n=30, seed=4)
+    B = rng.standard_normal((30, 2))
+    r = orc.mbcg_dense(A, B, 30, tol=1e-6)
+    for col in range(2):
+        it = r["iters"][col]
+        assert it < 30 and r["relres_hist"][it - 1, col] < 1e-6
+        assert np.all(r["relres_hist"][it:, col] == 0.0)
+
+
+def test_preconditioning_lowers_residual(orc):
+    # the paper's claim for pivoted-Cholesky preconditioning of smooth kernels:
+    # at a fixed iteration the rank-k preconditioned residual is far below the plain one
+    rng = np.random.default_rng(5)
+    X = rng.random((200, 1))
+    K = ref.kernel_matrix(ref.RBF, X, X, math.log(0.2), 0.0)
+    A = K + 0.01 * np.eye(200)
+    B = rng.standard_normal((200, 1))
+    L, piv, ku, _ = orc.pivchol_dense(K, 12)
+    plain = orc.mbcg_dense(A, B, 10)["relres_hist"][:, 0]
+    pre = orc.mbcg_dense(A, B, 10, L=L[:, :ku], noise_var=0.01)["relres_hist"][:, 0]
+    assert pre[9] < 1e-2 * plain[9], (pre[9], plain[9])
