@@ -177,14 +177,16 @@ bbmm_status_t bbmm_pivchol(bbmm_ctx_t ctx, const float *X_d, int64_t n,
  *   exactly max_iter iterations.  1 <= ncols <= 64.
  *   alpha_h, beta_h: max_iter x ncols host fp64 (row j = iteration j; 0 where
  *   not computed);  iters_h: ncols int32 (alphas recorded per column);
- *   relres_h: ncols fp64;  rho0_h: ncols fp64 (b^T Phat^{-1} b), may be NULL. */
+ *   relres_h: ncols fp64;  rho0_h: ncols fp64 (b^T Phat^{-1} b), may be NULL;
+ *   relres_hist_h: max_iter x ncols fp64, row j = ||r_c|| / ||b_c|| after
+ *   iteration j (0 once the column is frozen), may be NULL (row f3 study). */
 bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X_d, int64_t n, int32_t d,
                         const bbmm_hyper_t *hyper, bbmm_kmode_t kmode,
                         const double *L_d, int32_t k, const double *B_d,
                         int32_t ncols, int64_t ldb, int32_t max_iter,
                         double tol, double *U_d, int64_t ldu, double *alpha_h,
                         double *beta_h, int32_t *iters_h, double *relres_h,
-                        double *rho0_h);
+                        double *rho0_h, double *relres_hist_h);
 
 /* One-call exact-GP marginal log likelihood and gradient (north-star entry):
  *   pivchol(k) -> Phat -> probes z_i = L eps1_i + sigma eps2_i (k >= 1; plain

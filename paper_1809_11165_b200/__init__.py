@@ -79,7 +79,7 @@ _lib.bbmm_kernel_matmul.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, 
 _lib.bbmm_pivchol.argtypes = [_p, _p, _i64, _i32, _HP, _i32, _p, _p, C.POINTER(_i32),
                               C.POINTER(_d)]
 _lib.bbmm_mbcg.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _p, _i32, _i64, _i32, _d,
-                           _p, _i64, _p, _p, _p, _p, _p]
+                           _p, _i64, _p, _p, _p, _p, _p, _p]
 _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d,
                                    _u64, _p, C.POINTER(_d), _p, C.POINTER(Stats), _p, _p]
 _lib.bbmm_predict.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d, _p, _p]
@@ -244,13 +244,15 @@ def mbcg(ctx: Context, X, hyper: Hyper, B, L=None, max_iter: int = 20, tol: floa
     it = np.zeros(c, np.int32)
     rr = np.zeros(c)
     r0 = np.zeros(c)
+    rh = np.zeros((max_iter, c))
     hp = hyper._c()
     Lp = _dev(L, torch.float64, "L", ctx) if k > 0 else None
     ctx.check(_lib.bbmm_mbcg(ctx._h, _dev(X, torch.float32, "X", ctx), n, d, C.byref(hp), kmode,
                              Lp, k, _dev(B, torch.float64, "B", ctx), c, c, max_iter, float(tol),
                              _p(U.data_ptr()), c, al.ctypes.data_as(_p), be.ctypes.data_as(_p),
-                             it.ctypes.data_as(_p), rr.ctypes.data_as(_p), r0.ctypes.data_as(_p)))
-    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0)
+                             it.ctypes.data_as(_p), rr.ctypes.data_as(_p), r0.ctypes.data_as(_p),
+                             rh.ctypes.data_as(_p)))
+    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0, relres_hist=rh)
 
 
 def mll_and_grad(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int = 20,

@@ -458,7 +458,7 @@ bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
                         const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, const double *L, int32_t k,
                         const double *B, int32_t ncols, int64_t ldb, int32_t max_iter, double tol,
                         double *U, int64_t ldu, double *alpha_h, double *beta_h, int32_t *iters_h,
-                        double *relres_h, double *rho0_h) {
+                        double *relres_h, double *rho0_h, double *relres_hist_h) {
     return guarded(ctx, [&] {
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
@@ -495,6 +495,7 @@ bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
         if (iters_h) std::copy(o.iters.begin(), o.iters.end(), iters_h);
         if (relres_h) std::copy(o.relres.begin(), o.relres.end(), relres_h);
         if (rho0_h) std::copy(o.rho0.begin(), o.rho0.end(), rho0_h);
+        if (relres_hist_h) std::copy(o.relres_hist.begin(), o.relres_hist.end(), relres_hist_h);
     });
 }
 

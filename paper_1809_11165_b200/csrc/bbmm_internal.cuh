@@ -195,6 +195,7 @@ struct MbcgOut {
     const double *bhist_d = nullptr;
     const MbcgState *state_d = nullptr;
     std::vector<double> alpha, beta, relres, rho0;
+    std::vector<double> relres_hist;   // max_iter x c: relres after each iteration (0: frozen)
     std::vector<int> iters;
     int iters_run = 0;
     float ms_matmul = 0.f;

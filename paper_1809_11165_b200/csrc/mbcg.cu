@@ -291,12 +291,14 @@ __global__ void k_passB(const MbcgState *__restrict__ st, const double *__restri
 // relres, freezing (relres < tol, reading R9), then S = C^{-1} W.
 // red layout: [rr (c) | W (k*c)].
 __global__ void k_after_B(MbcgState *st, const double *__restrict__ red, const double *cholC,
-                          int k, int c, double tol, double *__restrict__ S) {
+                          int k, int c, double tol, double *__restrict__ S,
+                          double *__restrict__ rhist) {
     const int col = threadIdx.x;
     if (col >= c) return;
     if (st->active[col]) {
         double rel = sqrt(red[col]) / st->bnorm[col];
         st->relres[col] = rel;
+        rhist[(int64_t)st->j * c + col] = rel;          // relres after iteration j (row f3)
         if (rel < tol) st->active[col] = 0;
     }
     if (k > 0) chol_solve_col(cholC, k, red + c, S, c, col);
@@ -541,6 +543,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     double *S = (double *)ws.get("cg_S", (size_t)kk * c * 8);
     MbcgState *st = (MbcgState *)ws.get("cg_state", sizeof(MbcgState));
     double *ahist = (double *)ws.get("cg_ahist", (size_t)a.max_iter * c * 8);
+    double *rhist = (double *)ws.get("cg_rhist", (size_t)a.max_iter * c * 8);
+    BBMM_CUDA(cudaMemsetAsync(rhist, 0, (size_t)a.max_iter * c * 8, sm));
     double *bhist = (double *)ws.get("cg_bhist", (size_t)a.max_iter * c * 8);
     BBMM_CUDA(cudaMemsetAsync(ahist, 0, (size_t)a.max_iter * c * 8, sm));
     BBMM_CUDA(cudaMemsetAsync(bhist, 0, (size_t)a.max_iter * c * 8, sm));
@@ -653,7 +657,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         reduce(c, red);
         LtR(red + c);
         if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
-        k_after_B<<<1, 64, 0, sm>>>(st, red, cholC, k, c, a.tol, S);
+        k_after_B<<<1, 64, 0, sm>>>(st, red, cholC, k, c, a.tol, S, rhist);
         precond_apply(red_rz);
         if (multi) allreduce_sum(ctx, red_rz, c);
         k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
@@ -676,6 +680,9 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     MbcgState st_h;
     out.alpha.assign((size_t)a.max_iter * c, 0.0);
     out.beta.assign((size_t)a.max_iter * c, 0.0);
+    out.relres_hist.assign((size_t)a.max_iter * c, 0.0);
+    BBMM_CUDA(cudaMemcpyAsync(out.relres_hist.data(), rhist, (size_t)a.max_iter * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
     BBMM_CUDA(cudaMemcpyAsync(out.alpha.data(), ahist, (size_t)a.max_iter * c * 8,
                               cudaMemcpyDeviceToHost, sm));
     BBMM_CUDA(cudaMemcpyAsync(out.beta.data(), bhist, (size_t)a.max_iter * c * 8,
