@@ -102,6 +102,13 @@ def _declare(L):
     L.orc_train_adam.argtypes = [_i, _p, _p, _i64, _i, _i, _p, _i, _i, _i, _d, _u64, _i, _d, _d,
                                  _d, _d, _p, _p]
     L.orc_train_adam.restype = _i
+    L.orc_sor_matmul.argtypes = [_i, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _p, _i, _i, _p]
+    L.orc_sor_matmul.restype = _i
+    L.orc_pivchol_sor.argtypes = [_i, _p, _i64, _i, _p, _i64, _i, _p, _d, _i, _p, _p, _p, _p]
+    L.orc_pivchol_sor.restype = _i
+    L.orc_mbcg_sor.argtypes = [_i, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _p, _i, _p, _i, _i, _d,
+                               _p, _p, _p, _p, _p, _p, _p]
+    L.orc_mbcg_sor.restype = _i
     L.orc_num_threads.argtypes = []
 
 
@@ -375,3 +382,48 @@ def train_adam(kind, X, y, log_ls, log_s, log_noise, t, k, p, steps, lr=0.1, b1=
                                 int(seed) & (2**64 - 1), steps, float(lr), float(b1), float(b2),
                                 float(eps), _ptr(out), _ptr(trace)), "train_adam")
     return out, trace[:steps]
+
+
+# ------------------------------------------------------- SoR operator (row f4)
+def sor_matmul(kind, X, Xu, log_ls, log_s, log_noise, M, with_noise=True):
+    """K_SoR M (+ sigma^2 M): K_SoR = K_XU (K_UU + 1e-6 s I)^{-1} K_UX (reading R28)."""
+    X, Xu = _f32(X), _f32(Xu)
+    n, d = X.shape
+    m = Xu.shape[0]
+    M = _f64(M).reshape(n, -1)
+    c = M.shape[1]
+    lls = _f64(np.atleast_1d(log_ls))
+    out = np.zeros((n, c))
+    _check(lib().orc_sor_matmul(kind, _ptr(X), n, d, _ptr(Xu), m, lls.size, _ptr(lls), float(log_s),
+                                float(log_noise), _ptr(M), c, int(with_noise), _ptr(out)),
+           "sor_matmul")
+    return out
+
+
+def pivchol_sor(kind, X, Xu, log_ls, log_s, k):
+    X, Xu = _f32(X), _f32(Xu)
+    n, d = X.shape
+    lls = _f64(np.atleast_1d(log_ls))
+    L = np.zeros((n, max(k, 1)))
+    piv = np.full(max(k, 1), -1, np.int64)
+    ku, res = C.c_int(0), C.c_double(0)
+    _check(lib().orc_pivchol_sor(kind, _ptr(X), n, d, _ptr(Xu), Xu.shape[0], lls.size, _ptr(lls),
+                                 float(log_s), k, _ptr(L), _ptr(piv), C.byref(ku), C.byref(res)),
+           "pivchol_sor")
+    return L[:, :k], piv[:k], ku.value, res.value
+
+
+def mbcg_sor(kind, X, Xu, log_ls, log_s, log_noise, B, p, tol=0.0, L=None):
+    X, Xu = _f32(X), _f32(Xu)
+    n, d = X.shape
+    B = _f64(B).reshape(n, -1)
+    c = B.shape[1]
+    lls = _f64(np.atleast_1d(log_ls))
+    k = 0 if L is None else L.shape[1]
+    Lp = np.zeros((n, 1)) if L is None else _f64(L)
+    U, al, be, it, rr, r0, rh = _mbcg_out(n, c, p)
+    _check(lib().orc_mbcg_sor(kind, _ptr(X), n, d, _ptr(Xu), Xu.shape[0], lls.size, _ptr(lls),
+                              float(log_s), float(log_noise), _ptr(Lp), k, _ptr(B), c, p, float(tol),
+                              _ptr(U), _ptr(al), _ptr(be), _ptr(it), _ptr(rr), _ptr(r0), _ptr(rh)),
+           "mbcg_sor")
+    return dict(U=U, alpha=al, beta=be, iters=it, relres=rr, rho0=r0, relres_hist=rh)

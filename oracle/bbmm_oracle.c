@@ -978,6 +978,169 @@ int orc_train_adam(int kind, const float *X32, const float *y32, int64_t n, int 
     return st;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Row f4: the Subset-of-Regressors (SGPR) operator through the same mBCG     */
+/* ("Programmability"; row access for pivoted Cholesky, App. B      */
+/* P:156-171):                                                                */
+/*   K_SoR = K_XU (K_UU + j I)^{-1} K_UX ,  Khat_SoR = K_SoR + sigma^2 I       */
+/* with m inducing points U and jitter j = 1e-6 s (reading R28).  The oracle  */
+/* applies the definition: T = K_UX M, T = (K_UU + jI)^{-1} T (Cholesky       */
+/* solve), out = K_XU T (+ sigma^2 M).                                        */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    hyper_t h;
+    int64_t m;
+    double *Kxu;   /* n x m */
+    double *Luu;   /* m x m lower Cholesky factor of K_UU + j I */
+} sor_t;
+
+static int sor_init(sor_t *S, int kind, const double *X, int64_t n, int d, const double *U,
+                    int64_t m, int n_ls, const double *log_ls, double log_s, double log_noise)
+{
+    int st = hyper_init(&S->h, kind, X, n, d, n_ls, log_ls, log_s, log_noise);
+    if (st != ORC_OK) return st;
+    S->m = m;
+    S->Kxu = (double *)malloc(sizeof(double) * (size_t)n * m);
+    S->Luu = (double *)malloc(sizeof(double) * (size_t)m * m);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t a = 0; a < m; a++)
+            S->Kxu[i * m + a] = orc_kernel(kind, d, X + i * d, U + a * d, S->h.n_ls, S->h.ls, S->h.s);
+    for (int64_t a = 0; a < m; a++)
+        for (int64_t b = 0; b < m; b++)
+            S->Luu[a * m + b] = orc_kernel(kind, d, U + a * d, U + b * d, S->h.n_ls, S->h.ls, S->h.s)
+                                + (a == b ? 1e-6 * S->h.s : 0.0);
+    return chol_small(S->Luu, (int)m);
+}
+
+static void sor_free(sor_t *S) { free(S->Kxu); free(S->Luu); }
+
+/* x <- (L L^T)^{-1} x for the m x m factor L (c right-hand sides, x is m x c) */
+static void chol_solve_mc(const double *L, int64_t m, double *x, int c)
+{
+    for (int col = 0; col < c; col++) {
+        for (int64_t a = 0; a < m; a++) {
+            double s = x[a * c + col];
+            for (int64_t b = 0; b < a; b++) s -= L[a * m + b] * x[b * c + col];
+            x[a * c + col] = s / L[a * m + a];
+        }
+        for (int64_t a = m - 1; a >= 0; a--) {
+            double s = x[a * c + col];
+            for (int64_t b = a + 1; b < m; b++) s -= L[b * m + a] * x[b * c + col];
+            x[a * c + col] = s / L[a * m + a];
+        }
+    }
+}
+
+/* out = K_SoR M (+ sigma^2 M if with_noise), M n x c */
+static void sor_apply(const sor_t *S, const double *M, int c, double *out, int with_noise)
+{
+    const int64_t n = S->h.n, m = S->m;
+    double *T = (double *)calloc((size_t)m * c, sizeof(double));
+    for (int64_t i = 0; i < n; i++)
+        for (int64_t a = 0; a < m; a++)
+            for (int col = 0; col < c; col++) T[a * c + col] += S->Kxu[i * m + a] * M[i * c + col];
+    chol_solve_mc(S->Luu, m, T, c);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; i++)
+        for (int col = 0; col < c; col++) {
+            double s = 0.0;
+            for (int64_t a = 0; a < m; a++) s += S->Kxu[i * m + a] * T[a * c + col];
+            out[i * c + col] = with_noise ? s + S->h.noise_var * M[i * c + col] : s;
+        }
+    free(T);
+}
+
+static void sor_op(const void *ctx, const double *M, int c, double *out)
+{
+    sor_apply((const sor_t *)ctx, M, c, out, 1);
+}
+
+/* row i of K_SoR: K_XU (K_UU + jI)^{-1} k_{U x_i} */
+static void sor_row(const void *ctx, int64_t i, double *out)
+{
+    const sor_t *S = (const sor_t *)ctx;
+    const int64_t m = S->m;
+    double *w = (double *)malloc(sizeof(double) * m);
+    memcpy(w, S->Kxu + i * m, sizeof(double) * m);
+    chol_solve_mc(S->Luu, m, w, 1);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < S->h.n; j++) {
+        double s = 0.0;
+        for (int64_t a = 0; a < m; a++) s += S->Kxu[j * m + a] * w[a];
+        out[j] = s;
+    }
+    free(w);
+}
+
+int orc_sor_matmul(int kind, const float *X32, int64_t n, int d, const float *U32, int64_t m,
+                   int n_ls, const double *log_ls, double log_s, double log_noise,
+                   const double *M, int c, int with_noise, double *out)
+{
+    if (n < 1 || m < 1 || c < 1) return ORC_ERR_ARG;
+    double *X = upcast_X(X32, n, d), *U = upcast_X(U32, m, d);
+    sor_t S;
+    int st = sor_init(&S, kind, X, n, d, U, m, n_ls, log_ls, log_s, log_noise);
+    if (st == ORC_OK) sor_apply(&S, M, c, out, with_noise);
+    sor_free(&S); free(X); free(U);
+    return st;
+}
+
+/* pivoted Cholesky of K_SoR through its rows (App. B): diag_i = row_i[i] */
+static int pivchol_sor(const sor_t *S, int k, double *L, int64_t *piv, int *k_used, double *resid)
+{
+    const int64_t n = S->h.n, m = S->m;
+    double *diag = (double *)malloc(sizeof(double) * n);
+    double *w = (double *)malloc(sizeof(double) * m);
+    for (int64_t i = 0; i < n; i++) {
+        memcpy(w, S->Kxu + i * m, sizeof(double) * m);
+        chol_solve_mc(S->Luu, m, w, 1);
+        double s = 0.0;
+        for (int64_t a = 0; a < m; a++) s += S->Kxu[i * m + a] * w[a];
+        diag[i] = s;
+    }
+    int st = pivchol_generic(sor_row, S, diag, n, k, 1e-12 * S->h.s, L, piv, k_used, resid);
+    free(diag); free(w);
+    return st;
+}
+
+int orc_pivchol_sor(int kind, const float *X32, int64_t n, int d, const float *U32, int64_t m,
+                    int n_ls, const double *log_ls, double log_s, int k, double *L,
+                    int64_t *piv, int *k_used, double *resid)
+{
+    if (k < 0 || k > n) return ORC_ERR_ARG;
+    double *X = upcast_X(X32, n, d), *U = upcast_X(U32, m, d);
+    sor_t S;
+    int st = sor_init(&S, kind, X, n, d, U, m, n_ls, log_ls, log_s, 0.0);
+    if (st == ORC_OK) st = pivchol_sor(&S, k, L, piv, k_used, resid);
+    sor_free(&S); free(X); free(U);
+    return st;
+}
+
+/* mBCG on Khat_SoR with a preconditioner L (n x k, e.g. from orc_pivchol_sor) */
+int orc_mbcg_sor(int kind, const float *X32, int64_t n, int d, const float *U32, int64_t m,
+                 int n_ls, const double *log_ls, double log_s, double log_noise,
+                 const double *L, int k, const double *B, int c, int p, double tol,
+                 double *Uo, double *alpha, double *beta, int *iters, double *relres,
+                 double *rho0, double *relres_hist)
+{
+    double *X = upcast_X(X32, n, d), *U = upcast_X(U32, m, d);
+    sor_t S;
+    int st = sor_init(&S, kind, X, n, d, U, m, n_ls, log_ls, log_s, log_noise);
+    if (st == ORC_OK) {
+        precond_t P = {L, n, k, k > 0 ? k : -1, S.h.noise_var, NULL};
+        double ld;
+        P.cholC = (double *)malloc(sizeof(double) * (k > 0 ? k * k : 1));
+        st = orc_precond_setup(L, n, k, P.k, S.h.noise_var, P.cholC, &ld);
+        if (st == ORC_OK)
+            st = mbcg_generic(sor_op, &S, &P, n, B, c, p, tol, Uo, alpha, beta, iters, relres,
+                              rho0, relres_hist);
+        free(P.cholC);
+    }
+    sor_free(&S); free(X); free(U);
+    return st;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP
