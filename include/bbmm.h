@@ -251,6 +251,25 @@ bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X_d, const float *y_d
                               double beta2, double eps, double *theta_out_h,
                               double *trace_h);
 
+/* Second operator through the same mBCG (PAPER.md:786-799
+ * "Programmability", row access for pivoted Cholesky App. B): the
+ * Subset-of-Regressors / SGPR kernel with m inducing points U,
+ *   Khat_SoR = K_XU (K_UU + 1e-6 s I)^{-1} K_UX + sigma^2 I   (jitter: reading R28)
+ * Builds Bs = Lu^{-1} K_UX (K_UU + jI = Lu Lu^T; m x n fp64, every rank), the
+ * rank-k pivoted Cholesky of K_SoR = Bs^T Bs through its rows (k = 0: none), then
+ * one mBCG call on B exactly as bbmm_mbcg (B_d, U_d: local rows x ncols fp64).
+ * Xu_d: m x d fp32 device, 1 <= m <= 512.  piv_h (k int64), iters_h,
+ * relres_h (ncols), relres_hist_h (max_iter x ncols): host, may be NULL.
+ * Errors: BBMM_ERR_ARG (sizes / NULL), BBMM_ERR_DATA (non-finite X / Xu),
+ *   BBMM_ERR_NUMERIC (K_UU + jI not PD, mBCG breakdown). */
+bbmm_status_t bbmm_sor_mbcg(bbmm_ctx_t ctx, const float *X_d, int64_t n, int32_t d,
+                            const float *Xu_d, int32_t m,
+                            const bbmm_hyper_t *hyper, int32_t k, const double *B_d,
+                            int32_t ncols, int64_t ldb, int32_t max_iter,
+                            double tol, double *U_d, int64_t ldu, int64_t *piv_h,
+                            int32_t *iters_h, double *relres_h,
+                            double *relres_hist_h);
+
 #ifdef __cplusplus
 }
 #endif

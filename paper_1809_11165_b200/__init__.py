@@ -85,9 +85,11 @@ _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _
 _lib.bbmm_predict.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d, _p, _p]
 _lib.bbmm_train_adam.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d, _u64,
                                  _i32, _d, _d, _d, _d, _p, _p]
+_lib.bbmm_sor_mbcg.argtypes = [_p, _p, _i64, _i32, _p, _i32, _HP, _i32, _p, _i32, _i64, _i32, _d,
+                               _p, _i64, _p, _p, _p, _p]
 for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
            "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
-           "bbmm_mll_and_grad", "bbmm_predict", "bbmm_train_adam"):
+           "bbmm_mll_and_grad", "bbmm_predict", "bbmm_train_adam", "bbmm_sor_mbcg"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -321,3 +323,25 @@ def train_adam(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int =
                                    float(beta1), float(beta2), float(eps), th.ctypes.data_as(_p),
                                    trace.ctypes.data_as(_p)))
     return Hyper(hyper.kind, th[:nls], th[nls], th[nls + 1]), trace[:steps]
+
+
+def sor_mbcg(ctx: Context, X, Xu, hyper: Hyper, B, k: int = 0, max_iter: int = 20,
+             tol: float = 0.0):
+    """mBCG on the SoR / SGPR operator K_XU (K_UU + 1e-6 s I)^{-1} K_UX + sigma^2 I with a
+    rank-k pivoted-Cholesky preconditioner of K_SoR (bbmm_sor_mbcg)."""
+    torch = _torch()
+    n, d = X.shape
+    m = Xu.shape[0]
+    nl, c = B.shape
+    U = torch.empty_like(B)
+    piv = np.full(max(k, 1), -1, np.int64)
+    it = np.zeros(c, np.int32)
+    rr = np.zeros(c)
+    rh = np.zeros((max_iter, c))
+    hp = hyper._c()
+    ctx.check(_lib.bbmm_sor_mbcg(ctx._h, _dev(X, torch.float32, "X", ctx), n, d,
+                                 _dev(Xu, torch.float32, "Xu", ctx), m, C.byref(hp), k,
+                                 _dev(B, torch.float64, "B", ctx), c, c, max_iter, float(tol),
+                                 _p(U.data_ptr()), c, piv.ctypes.data_as(_p), it.ctypes.data_as(_p),
+                                 rr.ctypes.data_as(_p), rh.ctypes.data_as(_p)))
+    return dict(U=U, pivots=piv[:k], iters=it, relres=rr, relres_hist=rh)

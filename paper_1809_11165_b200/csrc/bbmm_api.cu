@@ -767,4 +767,48 @@ bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X, const float *y, in
     });
 }
 
+bbmm_status_t bbmm_sor_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d, const float *Xu,
+                            int32_t m, const bbmm_hyper_t *hyper, int32_t k, const double *B,
+                            int32_t ncols, int64_t ldb, int32_t max_iter, double tol, double *U,
+                            int64_t ldu, int64_t *piv_h, int32_t *iters_h, double *relres_h,
+                            double *relres_hist_h) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(Xu != nullptr && B != nullptr && U != nullptr, "Xu / B / U is NULL");
+        BBMM_REQUIRE(m >= 1 && m <= kMaxInducing, "m must be in [1, 512]");
+        BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
+        BBMM_REQUIRE(ncols >= 1 && ncols <= kMaxCols, "ncols must be in [1, 64]");
+        BBMM_REQUIRE(ldb >= ncols && ldu >= ncols, "leading dimension < ncols");
+        BBMM_REQUIRE(max_iter >= 1 && max_iter <= 256, "max_iter must be in [1, 256]");
+        BBMM_REQUIRE(tol >= 0.0 && std::isfinite(tol), "tol must be >= 0");
+        check_finite(ctx, X, n * d, "X");
+        check_finite(ctx, Xu, (int64_t)m * d, "Xu");
+        RowRange rr = local_rows(ctx, n);
+        const int64_t nloc = rr.count();
+        double *Bs = (double *)ctx->ws.get("sor_Bs", (size_t)m * n * 8);
+        sor_setup(ctx, X, n, d, Xu, m, h, Bs);
+        double *L = (double *)ctx->ws.get("L", (size_t)std::max(k, 1) * n * 8);
+        int k_used = 0;
+        double resid = 0.0;
+        std::vector<int64_t> piv(std::max(k, 1), -1);
+        if (k > 0) pivchol_sor(ctx, Bs, n, m, h.s, k, L, piv.data(), &k_used, &resid);
+        double *cholC = (double *)ctx->ws.get("cholC", (size_t)std::max(k, 1) * std::max(k, 1) * 8);
+        double *ldp = (double *)ctx->ws.get("logdet_pre", 8);
+        precond_setup(ctx, L, n, k > 0 ? k_used : 0, h.noise_var, cholC, ldp);
+        MbcgArgs a{nullptr, 0, h.kind, h.s, TcOperand{}, nullptr, n, rr.r0, nloc, rr.nb,
+                   h.noise_var, L, k > 0 ? k_used : 0, ncols, max_iter, tol};
+        a.sor_B = Bs;
+        a.sor_m = m;
+        MbcgOut o;
+        o.U = U;
+        o.ldu = ldu;
+        mbcg_run(ctx, a, B, ldb, cholC, o);
+        if (piv_h) std::copy(piv.begin(), piv.begin() + k, piv_h);
+        if (iters_h) std::copy(o.iters.begin(), o.iters.end(), iters_h);
+        if (relres_h) std::copy(o.relres.begin(), o.relres.end(), relres_h);
+        if (relres_hist_h) std::copy(o.relres_hist.begin(), o.relres_hist.end(), relres_hist_h);
+    });
+}
+
 }  // extern "C"

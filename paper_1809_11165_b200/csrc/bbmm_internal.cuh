@@ -15,6 +15,7 @@
 namespace bbmm {
 
 constexpr int kMaxCols = 64;     // ncols = t + 1 <= 64
+constexpr int kMaxInducing = 512;  // SoR operator: inducing points m (row f4)
 constexpr int kMaxRank = 128;    // preconditioner rank k
 constexpr int kMaxDim = 32;      // input dimension d
 constexpr int kNumSMs = 148;
@@ -184,6 +185,7 @@ struct MbcgArgs {
     const double *L; int k;                         // k x n (full), k == 0: no precond
     int c;                                          // columns
     int max_iter; double tol;
+    const double *sor_B = nullptr; int sor_m = 0;   // SoR operator Bs (m x n), row f4
 };
 struct MbcgOut {
     double *U = nullptr; int64_t ldu = 0;   // optional copy of the solves
@@ -203,6 +205,12 @@ struct MbcgOut {
 };
 void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
                    double *cholC, double *logdet_d);
+// sor.cu: Bs = Lu^{-1} K_UX (m x n fp64, replicated), K_SoR = Bs^T Bs
+void sor_setup(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const float *U, int m,
+               const Hyper &h, double *Bs);
+// pivchol.cu: rank-k pivoted Cholesky of K_SoR = Bs^T Bs through its rows
+void pivchol_sor(bbmm_ctx_s *ctx, const double *Bs, int64_t n, int m, double s, int k, double *L,
+                 int64_t *piv_h, int *k_used_h, double *resid_h);
 // predict.cu: mean and pointwise variance (var may be null)
 void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
                  const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,

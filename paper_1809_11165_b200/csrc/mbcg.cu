@@ -150,6 +150,33 @@ __device__ void chol_solve_col(const double *__restrict__ cholC, int k, const do
     }
 }
 
+// SoR operator (row f4): Vpart[i][col] = sum_a Bs[a][r0 + i] T[a][col] (= K_SoR D on the
+// local rows; k_passA adds sigma^2 D).  Thread = one row x a chunk of 8 columns
+// (blockIdx.y); Bs reads coalesced across the warp, T from shared memory.
+__global__ void __launch_bounds__(256)
+k_sor_expand(const double *__restrict__ Bs, int64_t n, int64_t r0, int m,
+             const double *__restrict__ T, int64_t nloc, int c, int cs, double *__restrict__ Vpart) {
+    extern __shared__ double Tsm[];   // m x c
+    for (int e = threadIdx.x; e < m * c; e += blockDim.x) Tsm[e] = T[e];
+    __syncthreads();
+    const int c0 = blockIdx.y * 8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = 0.0;
+        for (int a = 0; a < m; a++) {
+            const double b = Bs[(int64_t)a * n + r0 + i];
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (c0 + u < c) acc[u] = fma(b, Tsm[a * c + c0 + u], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (c0 + u < c) Vpart[i * cs + c0 + u] = acc[u];
+    }
+}
+
 // Z = (R - L S)/sigma^2  (k >= 1) or Z = R (no preconditioner); partial <R,Z>.
 // Thread = one row x a chunk of 8 columns (blockIdx.y): L[m][row] loads are
 // coalesced across the warp, S comes from shared memory (broadcast).  The
@@ -528,8 +555,10 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     const bool acc64 = ctx->matmul_acc64;
     const size_t esz = acc64 ? 8 : 4;
     void *Dm = ws.get("cg_Dm", (size_t)npad * cs * esz);
-    const bool use_tc = a.tc.version != 0;
-    size_t vcap = use_tc ? tc_vpart_elems(a.tc, a.n, nloc, c) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
+    const bool use_sor = a.sor_B != nullptr;
+    const bool use_tc = a.tc.version != 0 && !use_sor;
+    size_t vcap = use_sor ? (size_t)std::max<int64_t>(nloc, 1) * cs
+                 : use_tc ? tc_vpart_elems(a.tc, a.n, nloc, c) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
     const int64_t npad_tc = use_tc ? k1tc_pad_rows(npad) : 0;
     uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(c)) : nullptr;
     double *Stc = use_tc ? (double *)ws.get("tc_S", kMaxCols * 8) : nullptr;
@@ -576,6 +605,42 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             part_ltr, ltr_blocks, k * c, dst);
         launches += 2;
     };
+    // SoR operator (row f4): T = Bs[:, local] D (the L^T R kernel with L = Bs), all-reduced,
+    // then Vpart = Bs[:, local]^T T; splits = 1
+    const int msor = use_sor ? a.sor_m : 1;
+    const size_t smem_sor = ((size_t)kLtrRows * c + (size_t)msor * c) * 8;
+    double *part_sor = use_sor ? (double *)ws.get("cg_part_sor", (size_t)ltr_blocks * msor * c * 8)
+                               : nullptr;
+    double *Tsor = use_sor ? (double *)ws.get("cg_Tsor", (size_t)msor * c * 8) : nullptr;
+    if (use_sor) {
+        if (smem_sor > 48 * 1024)
+            BBMM_CUDA(cudaFuncSetAttribute(ltr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)std::max(smem_sor, smem_ltr)));
+        if ((size_t)msor * c * 8 > 48 * 1024)
+            BBMM_CUDA(cudaFuncSetAttribute(k_sor_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)((size_t)msor * c * 8)));
+    }
+    auto sor_matmul = [&](cudaEvent_t e0, cudaEvent_t e1) {
+        if (e0) BBMM_CUDA(cudaEventRecord(e0, sm));
+        if (nloc > 0) {
+            ltr_kernel<<<ltr_blocks, 256, smem_sor, sm>>>(a.sor_B, a.n, a.r0, msor, D, nloc, c,
+                                                          part_sor);
+            k_reduce_blocks<<<std::max(1, (int)ceil_div(msor * c, 256)), 256, 0, sm>>>(
+                part_sor, ltr_blocks, msor * c, Tsor);
+            launches += 2;
+        } else {
+            BBMM_CUDA(cudaMemsetAsync(Tsor, 0, (size_t)msor * c * 8, sm));
+        }
+        if (multi) allreduce_sum(ctx, Tsor, (size_t)msor * c);
+        if (nloc > 0) {
+            const dim3 eg((unsigned)nblk, (unsigned)ceil_div(c, 8));
+            k_sor_expand<<<eg, 256, (size_t)msor * c * 8, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc,
+                                                               c, cs, Vpart);
+            launches++;
+        }
+        if (e1) BBMM_CUDA(cudaEventRecord(e1, sm));
+        return 1;
+    };
     // precondition apply: grid (row blocks, column chunks of 8); partials nblk x c
     const dim3 pa_grid((unsigned)nblk, (unsigned)ceil_div(c, 8));
     auto precond_apply = [&](double *dst) {
@@ -619,7 +684,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             if (multi) allreduce_max(ctx, Stc, c);
             if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp);
             if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * k1tc_bslice_rows(c));
-        } else if (multi) {
+        } else if (multi && !use_sor) {          // SoR needs only local rows of D
             allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
         }
     };
@@ -641,7 +706,9 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         mm_ev.push_back(e0);
         mm_ev.push_back(e1);
         int splits;
-        if (use_tc)
+        if (use_sor)
+            splits = sor_matmul(e0, e1);
+        else if (use_tc)
             splits = tc_matmul(ctx, a.tc, Bp, Stc, c, a.n, a.r0, nloc, a.s, Vpart, vcap, e0, e1);
         else if (a.Kst)
             splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, Dm, acc64, cp, Vpart, vcap, e0,

@@ -137,6 +137,58 @@ k_piv_step(PivState *st, int m, int kind, const float *__restrict__ X, int64_t n
     block_argmax(bv, bi, pv + blockIdx.x, pi + blockIdx.x);
 }
 
+// ---- SoR operator (row f4): rows of K_SoR = Bs^T Bs (Bs m x n, row-major)
+__global__ void __launch_bounds__(kThreads)
+k_piv_init_sor(double *__restrict__ diag, int64_t n, const double *__restrict__ Bs, int m,
+               double *__restrict__ L, int64_t Ltotal, PivState *st, double *pv, int64_t *pi) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < Ltotal;
+         e += (int64_t)gridDim.x * blockDim.x)
+        L[e] = 0.0;
+    double bv = -1.0;
+    int64_t bi = n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int a = 0; a < m; a++) {
+            const double b = Bs[(int64_t)a * n + i];
+            s = __dadd_rn(s, __dmul_rn(b, b));
+        }
+        diag[i] = s;
+        argmax_combine(bv, bi, s, i);
+    }
+    block_argmax(bv, bi, pv + blockIdx.x, pi + blockIdx.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->k_used = 0;
+        st->stop = 0;
+        st->pivval = 0.0;
+        for (int q = 0; q < kMaxRank; q++) st->piv[q] = -1;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_piv_step_sor(PivState *st, int mstep, const double *__restrict__ Bs, int m, int64_t n,
+               double *__restrict__ L, double *__restrict__ diag, double *pv, int64_t *pi) {
+    if (st->stop) return;
+    const int64_t p = st->piv[mstep];
+    const double sq = __dsqrt_rn(st->pivval);
+    double bv = -1.0;
+    int64_t bi = n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;                              // K_SoR[p][i] = Bs[:, p] . Bs[:, i]
+        for (int a = 0; a < m; a++)
+            acc = __dadd_rn(acc, __dmul_rn(Bs[(int64_t)a * n + p], Bs[(int64_t)a * n + i]));
+        for (int mm = 0; mm < mstep; mm++)
+            acc = __dsub_rn(acc, __dmul_rn(L[(int64_t)mm * n + i], L[(int64_t)mm * n + p]));
+        const double lim = __ddiv_rn(acc, sq);
+        L[(int64_t)mstep * n + i] = lim;
+        const double dg = (i == p) ? 0.0 : __dsub_rn(diag[i], __dmul_rn(lim, lim));
+        diag[i] = dg;
+        argmax_combine(bv, bi, dg, i);
+    }
+    block_argmax(bv, bi, pv + blockIdx.x, pi + blockIdx.x);
+}
+
 __global__ void k_sum(const double *__restrict__ x, int64_t n, double *out) {
     __shared__ double sh[kThreads];
     double acc = 0.0;
@@ -187,6 +239,41 @@ void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, 
     if (k == 0) res = h.s * (double)n;
     if (piv_h)
         for (int m = 0; m < k; m++) piv_h[m] = m < st_h.k_used ? st_h.piv[m] : -1;
+    if (k_used_h) *k_used_h = (k == 0) ? 0 : st_h.k_used;
+    if (resid_h) *resid_h = res;
+}
+
+void pivchol_sor(bbmm_ctx_s *ctx, const double *Bs, int64_t n, int m, double s, int k, double *L,
+                 int64_t *piv_h, int *k_used_h, double *resid_h) {
+    BBMM_REQUIRE(k >= 0 && k <= kMaxRank && k <= n, "pivchol rank out of range");
+    cudaStream_t sm = ctx->stream;
+    Workspace &ws = ctx->ws;
+    double *diag = (double *)ws.get("pv_diag", (size_t)n * 8);
+    PivState *st = (PivState *)ws.get("pv_state", sizeof(PivState));
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kThreads), 4 * kNumSMs));
+    double *pv = (double *)ws.get("pv_pv", (size_t)nblk * 8);
+    int64_t *pi = (int64_t *)ws.get("pv_pi", (size_t)nblk * 8);
+    double *res_d = (double *)ws.get("pv_res", 8);
+    const int64_t Ltot = (int64_t)std::max(k, 1) * n;
+    k_piv_init_sor<<<nblk, kThreads, 0, sm>>>(diag, n, Bs, m, L, k > 0 ? Ltot : 0, st, pv, pi);
+    int launches = 1;
+    const double stop_tol = 1e-12 * s;                 // as for the exact kernel (R23)
+    for (int q = 0; q < k; q++) {
+        k_piv_select<<<1, 32, 0, sm>>>(st, pv, pi, nblk, q, stop_tol);
+        k_piv_step_sor<<<nblk, kThreads, 0, sm>>>(st, q, Bs, m, n, L, diag, pv, pi);
+        launches += 2;
+    }
+    k_sum<<<1, kThreads, 0, sm>>>(diag, n, res_d);
+    launches++;
+    BBMM_LAUNCH_CHECK();
+    ctx->launches += launches;
+    PivState st_h;
+    BBMM_CUDA(cudaMemcpyAsync(&st_h, st, sizeof(PivState), cudaMemcpyDeviceToHost, sm));
+    double res = 0.0;
+    BBMM_CUDA(cudaMemcpyAsync(&res, res_d, 8, cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaStreamSynchronize(sm));
+    if (piv_h)
+        for (int q = 0; q < k; q++) piv_h[q] = q < st_h.k_used ? st_h.piv[q] : -1;
     if (k_used_h) *k_used_h = (k == 0) ? 0 : st_h.k_used;
     if (resid_h) *resid_h = res;
 }
