@@ -134,6 +134,68 @@ k_LtR(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *
     for (int e = tid; e < k * c; e += 256) part[(int64_t)blockIdx.x * k * c + e] = acc[e];
 }
 
+// Split-K register-tiled version of the same product (used when it fits): block b
+// owns a contiguous range of rows and ALL k x c outputs; thread t owns the column
+// group g = t % CGN (4 columns) and the rows m = t / CGN + j * MLN (j < MPT) of W,
+// accumulated in registers over the whole range -- one write per output, no
+// shuffles.  Per 16/32-row step the L tile (k x KT, stored transposed) and the
+// R tile are staged in shared memory; L reads are coalesced along the rows.
+template <int MPT>
+__global__ void __launch_bounds__(256, 2)
+k_LtR2(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *__restrict__ R,
+       int64_t nloc, int c, int64_t rows_per_blk, int KT, double *__restrict__ part) {
+    extern __shared__ double sm_l2[];
+    double *Lt = sm_l2;                           // KT x k  (Lt[kk * k + m])
+    double *Rt = Lt + (size_t)KT * k;             // KT x c
+    const int CGN = (c + 3) / 4, MLN = 256 / CGN;
+    const int g = threadIdx.x % CGN, ml = threadIdx.x / CGN;
+    const bool act = ml < MLN;
+    double acc[MPT][4];
+#pragma unroll
+    for (int j = 0; j < MPT; j++)
+#pragma unroll
+        for (int u = 0; u < 4; u++) acc[j][u] = 0.0;
+    const int64_t i_beg = (int64_t)blockIdx.x * rows_per_blk;
+    const int64_t i_end = min(nloc, i_beg + rows_per_blk);
+    for (int64_t i0 = i_beg; i0 < i_end; i0 += KT) {
+        const int rows = (int)min((int64_t)KT, i_end - i0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < k * KT; e += 256) {
+            const int m = e / KT, kk = e - m * KT;
+            Lt[kk * k + m] = kk < rows ? L[(int64_t)m * n + r0 + i0 + kk] : 0.0;
+        }
+        for (int e = threadIdx.x; e < KT * c; e += 256) {
+            const int kk = e / c;
+            Rt[e] = kk < rows ? R[i0 * c + e] : 0.0;
+        }
+        __syncthreads();
+        if (act) {
+            for (int kk = 0; kk < KT; kk++) {
+                double r[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) r[u] = (4 * g + u < c) ? Rt[kk * c + 4 * g + u] : 0.0;
+#pragma unroll
+                for (int j = 0; j < MPT; j++) {
+                    const int m = ml + j * MLN;
+                    const double l = m < k ? Lt[kk * k + m] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[j][u] = fma(l, r[u], acc[j][u]);
+                }
+            }
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int j = 0; j < MPT; j++) {
+            const int m = ml + j * MLN;
+            if (m < k)
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (4 * g + u < c) part[(int64_t)blockIdx.x * k * c + m * c + 4 * g + u] = acc[j][u];
+        }
+    }
+}
+
 // S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One block,
 // thread per column: forward then backward substitution.
 __device__ void chol_solve_col(const double *__restrict__ cholC, int k, const double *W, double *S,
@@ -151,29 +213,29 @@ __device__ void chol_solve_col(const double *__restrict__ cholC, int k, const do
 }
 
 // SoR operator (row f4): Vpart[i][col] = sum_a Bs[a][r0 + i] T[a][col] (= K_SoR D on the
-// local rows; k_passA adds sigma^2 D).  Thread = one row x a chunk of 8 columns
-// (blockIdx.y); Bs reads coalesced across the warp, T from shared memory.
+// local rows; k_passA adds sigma^2 D).  Thread = one row, all columns in registers (Bs
+// read once, coalesced across the warp); T from shared memory (broadcast).
+template <int CMAX>
 __global__ void __launch_bounds__(256)
 k_sor_expand(const double *__restrict__ Bs, int64_t n, int64_t r0, int m,
              const double *__restrict__ T, int64_t nloc, int c, int cs, double *__restrict__ Vpart) {
     extern __shared__ double Tsm[];   // m x c
     for (int e = threadIdx.x; e < m * c; e += blockDim.x) Tsm[e] = T[e];
     __syncthreads();
-    const int c0 = blockIdx.y * 8;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double acc[8];
+        double acc[CMAX];
 #pragma unroll
-        for (int u = 0; u < 8; u++) acc[u] = 0.0;
+        for (int u = 0; u < CMAX; u++) acc[u] = 0.0;
         for (int a = 0; a < m; a++) {
             const double b = Bs[(int64_t)a * n + r0 + i];
 #pragma unroll
-            for (int u = 0; u < 8; u++)
-                if (c0 + u < c) acc[u] = fma(b, Tsm[a * c + c0 + u], acc[u]);
+            for (int u = 0; u < CMAX; u++)
+                if (u < c) acc[u] = fma(b, Tsm[a * c + u], acc[u]);
         }
 #pragma unroll
-        for (int u = 0; u < 8; u++)
-            if (c0 + u < c) Vpart[i * cs + c0 + u] = acc[u];
+        for (int u = 0; u < CMAX; u++)
+            if (u < c) Vpart[i * cs + u] = acc[u];
     }
 }
 
@@ -598,9 +660,33 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         BBMM_CUDA(cudaFuncSetAttribute(ltr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_ltr));
     double *part_ltr = (double *)ws.get("cg_part_ltr", (size_t)ltr_blocks * kk * c * 8);
+    // part_out[blk][K x c] = Lp[:, rows of blk]^T R: the register-tiled split-K kernel when
+    // its per-thread tile fits (c <= 20, <= 16 rows of Lp per thread), else k_LtR
+    auto launch_ltr = [&](const double *Lp, int K, const double *Rp, double *part_out,
+                          size_t smem_fallback) {
+        const int CGN = (c + 3) / 4, MLN = 256 / CGN;
+        const int need = (K + MLN - 1) / MLN;
+        if (c <= 20 && need <= 16) {
+            const int KT = K <= 256 ? 32 : 16;
+            const int64_t rpb = ceil_div(ceil_div(std::max<int64_t>(nloc, 1), ltr_blocks), KT) * KT;
+            const size_t smem2 = ((size_t)KT * K + (size_t)KT * c) * 8;
+            static bool attr2 = false;
+            if (!attr2) {
+                for (auto f : {k_LtR2<1>, k_LtR2<2>, k_LtR2<4>, k_LtR2<8>, k_LtR2<12>, k_LtR2<16>})
+                    BBMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   100 * 1024));
+                attr2 = true;
+            }
+            auto f = need <= 1 ? k_LtR2<1> : need <= 2 ? k_LtR2<2> : need <= 4 ? k_LtR2<4>
+                   : need <= 8 ? k_LtR2<8> : need <= 12 ? k_LtR2<12> : k_LtR2<16>;
+            f<<<ltr_blocks, 256, smem2, sm>>>(Lp, a.n, a.r0, K, Rp, nloc, c, rpb, KT, part_out);
+        } else {
+            ltr_kernel<<<ltr_blocks, 256, smem_fallback, sm>>>(Lp, a.n, a.r0, K, Rp, nloc, c, part_out);
+        }
+    };
     auto LtR = [&](double *dst) {
         if (k == 0) return;
-        ltr_kernel<<<ltr_blocks, 256, smem_ltr, sm>>>(a.L, a.n, a.r0, k, R, nloc, c, part_ltr);
+        launch_ltr(a.L, k, R, part_ltr, smem_ltr);
         k_reduce_blocks<<<std::max(1, (int)ceil_div(k * c, 256)), 256, 0, sm>>>(
             part_ltr, ltr_blocks, k * c, dst);
         launches += 2;
@@ -608,6 +694,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     // SoR operator (row f4): T = Bs[:, local] D (the L^T R kernel with L = Bs), all-reduced,
     // then Vpart = Bs[:, local]^T T; splits = 1
     const int msor = use_sor ? a.sor_m : 1;
+    auto sor_expand = c <= 8 ? k_sor_expand<8> : (c <= 17 ? k_sor_expand<17>
+                    : (c <= 33 ? k_sor_expand<33> : k_sor_expand<kMaxCols>));
     const size_t smem_sor = ((size_t)kLtrRows * c + (size_t)msor * c) * 8;
     double *part_sor = use_sor ? (double *)ws.get("cg_part_sor", (size_t)ltr_blocks * msor * c * 8)
                                : nullptr;
@@ -617,14 +705,13 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             BBMM_CUDA(cudaFuncSetAttribute(ltr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)std::max(smem_sor, smem_ltr)));
         if ((size_t)msor * c * 8 > 48 * 1024)
-            BBMM_CUDA(cudaFuncSetAttribute(k_sor_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            BBMM_CUDA(cudaFuncSetAttribute(sor_expand, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)((size_t)msor * c * 8)));
     }
     auto sor_matmul = [&](cudaEvent_t e0, cudaEvent_t e1) {
         if (e0) BBMM_CUDA(cudaEventRecord(e0, sm));
         if (nloc > 0) {
-            ltr_kernel<<<ltr_blocks, 256, smem_sor, sm>>>(a.sor_B, a.n, a.r0, msor, D, nloc, c,
-                                                          part_sor);
+            launch_ltr(a.sor_B, msor, D, part_sor, smem_sor);
             k_reduce_blocks<<<std::max(1, (int)ceil_div(msor * c, 256)), 256, 0, sm>>>(
                 part_sor, ltr_blocks, msor * c, Tsor);
             launches += 2;
@@ -633,9 +720,9 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         }
         if (multi) allreduce_sum(ctx, Tsor, (size_t)msor * c);
         if (nloc > 0) {
-            const dim3 eg((unsigned)nblk, (unsigned)ceil_div(c, 8));
-            k_sor_expand<<<eg, 256, (size_t)msor * c * 8, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc,
-                                                               c, cs, Vpart);
+            const int eg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 4 * kNumSMs));
+            sor_expand<<<eg, 256, (size_t)msor * c * 8, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc, c,
+                                                             cs, Vpart);
             launches++;
         }
         if (e1) BBMM_CUDA(cudaEventRecord(e1, sm));

@@ -175,9 +175,17 @@ k_piv_step_sor(PivState *st, int mstep, const double *__restrict__ Bs, int m, in
     int64_t bi = n;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;                              // K_SoR[p][i] = Bs[:, p] . Bs[:, i]
-        for (int a = 0; a < m; a++)
-            acc = __dadd_rn(acc, __dmul_rn(Bs[(int64_t)a * n + p], Bs[(int64_t)a * n + i]));
+        // K_SoR[p][i] = Bs[:, p] . Bs[:, i], four partial sums (ILP over the strided loads)
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        int a = 0;
+        for (; a + 4 <= m; a += 4)
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                s4[u] = __dadd_rn(s4[u], __dmul_rn(Bs[(int64_t)(a + u) * n + p],
+                                                   Bs[(int64_t)(a + u) * n + i]));
+        for (; a < m; a++)
+            s4[0] = __dadd_rn(s4[0], __dmul_rn(Bs[(int64_t)a * n + p], Bs[(int64_t)a * n + i]));
+        double acc = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
         for (int mm = 0; mm < mstep; mm++)
             acc = __dsub_rn(acc, __dmul_rn(L[(int64_t)mm * n + i], L[(int64_t)mm * n + p]));
         const double lim = __ddiv_rn(acc, sq);
