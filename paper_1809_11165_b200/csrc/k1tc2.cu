@@ -314,13 +314,6 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::mbar_arrive(&init_done);
             for (int c = 0; c <= C; c++) acc_sm[c][rl] = 0.0;
         }
-#ifdef BBMM_TC2_STAGGER
-        if (h > 0) {
-            const long long c0 = clock64();
-            while (clock64() - c0 < (long long)h * BBMM_TC2_STAGGER) {
-            }
-        }
-#endif
         const uint32_t a_sfull = ptx::smem_u32(&s_full[0]);
         const uint32_t a_afull = ptx::smem_u32(&a_full[0]);
         const uint32_t a_accf = ptx::smem_u32(&acc_full), a_acce = ptx::smem_u32(&acc_empty);
