@@ -144,6 +144,26 @@ if "ldfirst" in abl:
     src = src.replace(a, b)
 if "n16" in abl:
     src = src.replace("constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);", "constexpr uint32_t IDQ = ptx::idesc_i8(BM, 16, false, false);")
+if "dist1" in abl or "dist2" in abl:
+    a = "for (int ks = 0; ks < 3 * DA / 8; ks++) {"
+    assert a in src
+    src = src.replace(a, "for (int ks = 0; ks < %d; ks++) {" % (1 if "dist1" in abl else 2))
+if "sttmlive" in abl:
+    # drop the A-slice stores but keep the quantised words live (no dead-code elimination)
+    for a_ in ("ptx::tmem_st4(col + 0,", "ptx::tmem_st4(col + 8,", "ptx::tmem_st4(col + 16,",
+               "ptx::tmem_st4(col + 4,", "ptx::tmem_st4(col + 12,", "ptx::tmem_st4(col + 20,"):
+        assert a_ in src, a_
+        src = src.replace(a_, "if (0) " + a_)
+    a_ = "            uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];"
+    assert a_ in src
+    src = src.replace(a_, a_ + "\n            uint32_t live_ = 0;")
+    a_ = "        if (ntl > 0) publish(ntl - 1);"
+    assert a_ in src
+    # fold every word into live_ at the end of each tile, store it only if impossible value
+    b_ = "            if constexpr (JW == 32) {\n                ptx::tmem_st4(col + 4"
+    src = src.replace("            if constexpr (JW == 32) {\n                if (0) ptx::tmem_st4(col + 4",
+                      "#pragma unroll\n            for (int u_ = 0; u_ < JW / 4; u_++) live_ ^= w0[u_] + w1[u_] * 3u + w2[u_] * 7u;\n            if (live_ == 0x9e3779b9u) Vpart[threadIdx.x] = (double)live_;\n            if constexpr (JW == 32) {\n                if (0) ptx::tmem_st4(col + 4")
+    assert "live_ ^=" in src
 f = os.path.join(ROOT, "scratch", "var_" + name, "k1tc2.cu")
 open(f, "w").write(src)
 subprocess.check_call([B.NVCC, "-std=c++17", "-O3", *B.ARCH, "-Xcompiler", "-fPIC", *defs, "-I", inc, "-I", B.CSRC,
