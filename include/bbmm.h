@@ -137,6 +137,12 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank,
                                 const void *nccl_unique_id_128_bytes);
 /* Select the matmul arithmetic for subsequent calls on ctx (default INT8EXACT). */
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p);
+/* Row partition of the multi-GPU path: rank owns
+ * [*r0, *r1) with blocks of nb = ceil(ceil(n / nranks) / 128) * 128 rows (host
+ * arithmetic only, no context or GPU needed; nb may be NULL).  BBMM_ERR_ARG for
+ * n < 0, nranks < 1, rank outside [0, nranks) or NULL outputs. */
+bbmm_status_t bbmm_row_partition(int64_t n, int32_t nranks, int32_t rank,
+                                 int64_t *r0, int64_t *r1, int64_t *nb);
 /* Local row range [*r0, *r1) of this rank for problem size n. */
 bbmm_status_t bbmm_local_rows(bbmm_ctx_t ctx, int64_t n, int64_t *r0,
                               int64_t *r1);

@@ -35,15 +35,17 @@ void Workspace::release_all() {
     bufs.clear();
 }
 
-RowRange local_rows(const bbmm_ctx_s *ctx, int64_t n) {
+// row blocks are multiples of 128 so rank boundaries align with the j-tiles of
+// the tensor-core operand (k1tc) and the all-gathers.
+static RowRange row_partition(int64_t n, int nranks, int rank) {
     RowRange r;
-    // row blocks are multiples of 128 so rank boundaries align with the
-    // j-tiles of the tensor-core operand (k1tc) and the all-gathers.
-    r.nb = ceil_div(ceil_div(n, ctx->nranks), 128) * 128;
-    r.r0 = std::min<int64_t>(n, (int64_t)ctx->rank * r.nb);
+    r.nb = ceil_div(ceil_div(n, nranks), 128) * 128;
+    r.r0 = std::min<int64_t>(n, (int64_t)rank * r.nb);
     r.r1 = std::min<int64_t>(n, r.r0 + r.nb);
     return r;
 }
+
+RowRange local_rows(const bbmm_ctx_s *ctx, int64_t n) { return row_partition(n, ctx->nranks, ctx->rank); }
 
 Hyper make_hyper(const bbmm_hyper_t *hp, int d) {
     BBMM_REQUIRE(hp != nullptr, "hyper is NULL");
@@ -359,6 +361,16 @@ bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precisio
         return BBMM_ERR_ARG;
     ctx->matmul_acc64 = (p != BBMM_MATMUL_FP32ACC);
     ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT);
+    return BBMM_OK;
+}
+
+bbmm_status_t bbmm_row_partition(int64_t n, int32_t nranks, int32_t rank, int64_t *r0,
+                                 int64_t *r1, int64_t *nb) {
+    if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !r0 || !r1) return BBMM_ERR_ARG;
+    const RowRange rr = row_partition(n, nranks, rank);
+    *r0 = rr.r0;
+    *r1 = rr.r1;
+    if (nb) *nb = rr.nb;
     return BBMM_OK;
 }
 

@@ -64,3 +64,26 @@ def test_oracle_not_imported_by_product():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "bbmm_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_row_partition_matches_python_mirror():
+    # the C partition (bbmm_row_partition, used by every multi-rank call) == the binding's
+    # row_partition used by the gloo multi-rank tests: contiguous, disjoint, covering,
+    # 128-aligned rank boundaries
+    lib = ctypes.CDLL(LIB)
+    lib.bbmm_row_partition.restype = ctypes.c_int
+    from paper_1809_11165_b200 import row_partition
+    r0, r1, nb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    for n in (0, 1, 127, 128, 129, 1000, 3338, 45730, 200000, 1000000, 1000003):
+        for G in (1, 2, 3, 4, 7, 8):
+            end = 0
+            for r in range(G):
+                st = lib.bbmm_row_partition(ctypes.c_int64(n), G, r, ctypes.byref(r0), ctypes.byref(r1),
+                                            ctypes.byref(nb))
+                assert st == 0
+                assert (r0.value, r1.value, nb.value) == tuple(row_partition(n, G, r))
+                assert r0.value == end and r1.value >= r0.value
+                assert r0.value % 128 == 0 or r0.value == n
+                end = r1.value
+            assert end == n
+    assert lib.bbmm_row_partition(ctypes.c_int64(10), 2, 2, ctypes.byref(r0), ctypes.byref(r1), None) != 0
