@@ -321,6 +321,7 @@ bbmm_status_t bbmm_ctx_destroy(bbmm_ctx_t ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->ws.release_all();
+    if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -100,6 +100,7 @@ struct bbmm_ctx_s {
     int launches = 0;   // library kernel launches since last reset
     bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
+    int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
 };
 
 namespace bbmm {

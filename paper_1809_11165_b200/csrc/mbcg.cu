@@ -468,19 +468,53 @@ __global__ void k_copy_U(const double *__restrict__ U, int64_t nloc, int c, doub
 }
 
 // ------------------------------------------------- preconditioner setup
-// C = sigma^2 I + L^T L (k x k) over all n rows, block partials.
-__global__ void k_LtL(const double *__restrict__ L, int64_t n, int k, double *__restrict__ part) {
-    const int64_t rows_per_blk = ceil_div(n, (int64_t)gridDim.x);
-    const int64_t i0 = (int64_t)blockIdx.x * rows_per_blk;
-    const int64_t i1 = min(n, i0 + rows_per_blk);
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-        int a = e / k, b = e - a * k;
-        if (b > a) continue;
-        const double *La = L + (int64_t)a * n, *Lb = L + (int64_t)b * n;
-        double acc = 0.0;
-        for (int64_t i = i0; i < i1; i++) acc += La[i] * Lb[i];
-        part[(int64_t)blockIdx.x * k * k + e] = acc;
+// C = sigma^2 I + L^T L (k x k).  Register-tiled L^T L over a row range (split-K): block b
+// sums rows [i_beg, i_end) of its share; thread (ta, tb) of a 16 x 16 grid owns C[a][b] for
+// a = ta + 16 p, b = tb + 16 q (p, q < KPT), accumulated in registers; L tiles (KT rows x k,
+// transposed) in shared memory.
+template <int KPT>
+__global__ void __launch_bounds__(256)
+k_LtL2(const double *__restrict__ L, int64_t n, int64_t r0, int64_t nrows, int k,
+       int64_t rows_per_blk, double *__restrict__ part) {
+    constexpr int KT = 16;
+    extern __shared__ double Lt[];            // KT x k
+    const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
+    double acc[KPT][KPT];
+#pragma unroll
+    for (int p = 0; p < KPT; p++)
+#pragma unroll
+        for (int q = 0; q < KPT; q++) acc[p][q] = 0.0;
+    const int64_t i_beg = (int64_t)blockIdx.x * rows_per_blk;
+    const int64_t i_end = min(nrows, i_beg + rows_per_blk);
+    for (int64_t i0 = i_beg; i0 < i_end; i0 += KT) {
+        const int rows = (int)min((int64_t)KT, i_end - i0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < k * KT; e += 256) {
+            const int m = e / KT, kk = e - m * KT;
+            Lt[kk * k + m] = kk < rows ? L[(int64_t)m * n + r0 + i0 + kk] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < KT; kk++) {
+            double va[KPT], vb[KPT];
+#pragma unroll
+            for (int p = 0; p < KPT; p++) {
+                const int a = ta + 16 * p, b = tb + 16 * p;
+                va[p] = a < k ? Lt[kk * k + a] : 0.0;
+                vb[p] = b < k ? Lt[kk * k + b] : 0.0;
+            }
+#pragma unroll
+            for (int p = 0; p < KPT; p++)
+#pragma unroll
+                for (int q = 0; q < KPT; q++) acc[p][q] = fma(va[p], vb[q], acc[p][q]);
+        }
     }
+#pragma unroll
+    for (int p = 0; p < KPT; p++)
+#pragma unroll
+        for (int q = 0; q < KPT; q++) {
+            const int a = ta + 16 * p, b = tb + 16 * q;
+            if (a < k && b < k) part[(int64_t)blockIdx.x * k * k + a * k + b] = acc[p][q];
+        }
 }
 
 // In-place Cholesky of C (k x k, lower) + log|P| = log|C| + (n-k) log sigma^2.
@@ -571,11 +605,23 @@ void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double no
         BBMM_CUDA(cudaMemsetAsync(logdet_d, 0, sizeof(double), ctx->stream));
         return;
     }
-    int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(kRedBlocks, ceil_div(n, 1024)));
+    // L^T L over this rank's rows (register-tiled split-K), then an all-reduce of the k x k sum
+    const RowRange rr = local_rows(ctx, n);
+    const int64_t nl = rr.count();
+    int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(std::max<int64_t>(nl, 1), 512)));
     double *part = (double *)ctx->ws.get("pc_part", sizeof(double) * nblk * k * k);
     double *red = (double *)ctx->ws.get("pc_red", sizeof(double) * k * k);
-    k_LtL<<<nblk, 256, 0, ctx->stream>>>(L, n, k, part);
-    k_reduce_blocks<<<ceil_div(k * k, 256), 256, 0, ctx->stream>>>(part, nblk, k * k, red);
+    const int kpt = (k + 15) / 16;
+    const int64_t rpb = ceil_div(ceil_div(std::max<int64_t>(nl, 1), nblk), 16) * 16;
+    const size_t smem = (size_t)16 * k * 8;
+    if (nl > 0) {
+        auto f = kpt <= 2 ? k_LtL2<2> : kpt <= 4 ? k_LtL2<4> : kpt <= 6 ? k_LtL2<6> : k_LtL2<8>;
+        f<<<nblk, 256, smem, ctx->stream>>>(L, n, rr.r0, nl, k, rpb, part);
+        k_reduce_blocks<<<ceil_div(k * k, 256), 256, 0, ctx->stream>>>(part, nblk, k * k, red);
+    } else {
+        BBMM_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * k * k, ctx->stream));
+    }
+    allreduce_sum(ctx, red, (size_t)k * k);
     k_chol_small<<<1, 32, 0, ctx->stream>>>(cholC, red, k, noise_var, n, logdet_d, status);
     BBMM_LAUNCH_CHECK();
     ctx->launches += 3;
@@ -783,8 +829,10 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     BBMM_CUDA(cudaEventCreate(&ev0));
     BBMM_CUDA(cudaEventCreate(&ev1));
     std::vector<cudaEvent_t> mm_ev;
-    int *any_h = nullptr;
-    BBMM_CUDA(cudaMallocHost(&any_h, sizeof(int)));
+    // pinned flag for convergence polling, allocated once per context and only when needed
+    // (cudaMallocHost costs tens of ms; with tol == 0 nothing is polled)
+    if (a.tol > 0.0 && !ctx->pinned_flag) BBMM_CUDA(cudaMallocHost(&ctx->pinned_flag, sizeof(int)));
+    int *any_h = ctx->pinned_flag;
     int iters_run = 0;
     for (int j = 0; j < a.max_iter; j++) {
         cudaEvent_t e0, e1;
@@ -854,7 +902,6 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     }
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    cudaFreeHost(any_h);
     out.ms_matmul = ms_tot;
     out.matmul_launches = iters_run;
     out.iters_run = iters_run;
