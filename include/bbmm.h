@@ -114,7 +114,9 @@ typedef struct {
     int32_t matmul_launches; /* K-hat*D kernel launches inside ms_matmul */
     int32_t gpu_launches;    /* library kernels launched by the call */
     int32_t matmul_path;     /* 0 on-the-fly CUDA-core (FP64ACC/FP32ACC),
-                                1 stored K, 2 tcgen05 exact (INT8EXACT) */
+                                1 stored fp32 K (FP64ACC/FP32ACC), 2 tcgen05 exact on the
+                                fly (INT8EXACT), 3 stored K as int8 slices on tcgen05
+                                (INT8EXACT, BBMM_STORED) */
     int32_t reserved_;
 } bbmm_stats_t;
 

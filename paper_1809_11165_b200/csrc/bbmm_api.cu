@@ -410,13 +410,15 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
         ctx->launches++;
         if (nloc == 0) return;
         const bool stored = kmode == BBMM_STORED;
-        TcOperand op = stored ? TcOperand{} : tc_prepare(ctx, X, n, d, ncols, h, n);
+        float *Kst = nullptr;
+        TcOperand op = prepare_operator(ctx, stored, X, Xs, dp, n, d, ncols, h, rr.r0, nloc, n, &Kst);
         if (op.version != 0) {
             const int64_t npad = k1tc_pad_rows(n);
             double *S = (double *)ctx->ws.get("tc_S", kMaxCols * 8);
             k1tc_colmax(ctx, D, ldd, n, ncols, S);
-            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * k1tc_bslice_rows(ncols));
-            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp);
+            const int nd = tc_dslices(op);
+            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * tc_bslice_rows(ncols, nd));
+            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp, nd);
             size_t cap = tc_vpart_elems(op, n, nloc, ncols);
             double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
             int splits = tc_matmul(ctx, op, Bp, S, ncols, n, rr.r0, nloc, h.s, Vpart, cap, nullptr,
@@ -432,9 +434,6 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
         double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
         int splits;
         if (stored) {
-            const int64_t ldk = ((n + 3) / 4) * 4;
-            float *Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
-            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
             splits = kernel_matmul_stored(ctx, Kst, n, nloc, Dm, acc64, cp, Vpart, cap, nullptr,
                                           nullptr);
         } else {
@@ -491,12 +490,8 @@ bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
         double *ldp = (double *)ctx->ws.get("logdet_pre", 8);
         precond_setup(ctx, L, n, k, h.noise_var, cholC, ldp);
         float *Kst = nullptr;
-        if (kmode == BBMM_STORED && nloc > 0) {
-            const int64_t ldk = ((n + 3) / 4) * 4;
-            Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
-            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
-        }
-        TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, ncols, h, rr.nb * ctx->nranks);
+        TcOperand tcop = prepare_operator(ctx, kmode == BBMM_STORED, X, Xs, dp, n, d, ncols, h,
+                                          rr.r0, nloc, rr.nb * ctx->nranks, &Kst);
         MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L, k, ncols,
                    max_iter, tol};
         MbcgOut o;
@@ -560,15 +555,10 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         if (nloc > 0)
             make_probes(ctx, eps, seed, n, k, t, L, k > 0 ? k_used : 0, k > 0 ? h.sigma : 1.0,
                         rr.r0, nloc, y, B, c);
-        float *Kst = nullptr;
-        if (kmode == BBMM_STORED && nloc > 0) {
-            const int64_t ldk = ((n + 3) / 4) * 4;
-            Kst = (float *)ws.get("Kst", (size_t)nloc * ldk * 4);
-            build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
-        }
-
         // 3. one mBCG call on [y, z_1..z_t]
-        TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, c, h, rr.nb * ctx->nranks);
+        float *Kst = nullptr;
+        TcOperand tcop = prepare_operator(ctx, kmode == BBMM_STORED, X, Xs, dp, n, d, c, h, rr.r0,
+                                          nloc, rr.nb * ctx->nranks, &Kst);
         MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
                    k > 0 ? k_used : 0, c, max_iter, tol};
         MbcgOut o;
@@ -707,7 +697,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             s.ms_deriv = t_end.since(t_slq);
             s.matmul_launches = o.matmul_launches;
             s.gpu_launches = ctx->launches - launches0;
-            s.matmul_path = tcop.version == 2 ? 2 : (Kst ? 1 : 0);
+            s.matmul_path = tcop.version == 3 ? 3 : tcop.version == 2 ? 2 : (Kst ? 1 : 0);
             *stats_h = s;
         }
         BBMM_CUDA(cudaStreamSynchronize(sm));

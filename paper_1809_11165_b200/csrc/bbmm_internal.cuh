@@ -144,7 +144,8 @@ int k1tc_bslice_rows(int c);
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean);
 void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, int c, double *S);
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
-               int64_t n, int c, const double *S, uint8_t *Bpack);
+               int64_t n, int c, const double *S, uint8_t *Bpack, int nd = 4);
+int tc_bslice_rows(int c, int nd);   // bytes per point of the packed D operand (nd slices)
 void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count);
 bool k1tc2_supported(int kind, int d, int c);
 int64_t k1tc2_xa_floats(int64_t npad, int d);
@@ -159,11 +160,13 @@ bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c);
 
 // Tensor-core operand of one mBCG call (prepared once per call).
 struct TcOperand {
-    int version = 0;            // 0: none (FP64ACC path), 2: k1tc2
+    int version = 0;            // 0: none (FP64ACC path), 2: k1tc2 (on the fly), 3: k2tc (stored)
     int d = 0;
     const float *Xa = nullptr;  // v2 row operand
     const float *XB = nullptr;  // v2 distance tiles
+    const uint8_t *Kq = nullptr;  // v3 stored K slices (this rank's rows)
 };
+int tc_dslices(const TcOperand &op);   // D slices of the operand's packed format (4 or 5)
 // Prepare the tensor-core inputs for (kind, d, c) if the INT8EXACT mode applies.
 TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, const Hyper &h,
                      int64_t npad_rows);
@@ -171,6 +174,21 @@ size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c);
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
               cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0);
+
+// stored K on the int8 tensor cores (k2tc.cu)
+bool k2tc_supported(int c);
+size_t k2tc_vpart_elems(int64_t n, int64_t nloc, int c);
+size_t k2tc_kq_bytes(int64_t n, int64_t nloc);
+void k2tc_build(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+                int64_t nloc, uint8_t *Kq);
+int k2tc_matmul(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const double *S, int c,
+                int64_t n, int64_t nloc, double s, double *Vpart, size_t cap, cudaEvent_t ev0,
+                cudaEvent_t ev1);
+// The operator of one call: on the fly -> tc_prepare; stored -> the int8 K slices (k2tc) when
+// INT8EXACT applies to c columns, else the fp32 stored K (*Kst, this rank's rows; null if none).
+TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const float *Xs, int dp,
+                           int64_t n, int d, int c, const Hyper &h, int64_t r0, int64_t nloc,
+                           int64_t npad_rows, float **Kst);
 
 // ------------------------------------------------------- pivchol.cu
 void pivchol(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h, int k,

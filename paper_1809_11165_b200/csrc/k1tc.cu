@@ -65,13 +65,17 @@ __global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c,
 
 // Pack rows [row0, row0 + rows) of D (fp64) into the K-major slice layout
 // [16-point chunk][NB rows][16 bytes] (linear in the chunk index, so any
-// multiple-of-16 j-tile is contiguous): row n = b_idx * BLK + col, b_idx 0..3
-// = bytes 3..0 of P' = round(D/S 2^30) + 2^30, col == c is the constant 2^30,
-// col > c zero padding.  One thread writes the 16 bytes of one (chunk, n).
+// multiple-of-16 j-tile is contiguous): row n = b_idx * BLK + col, b_idx
+// 0..ND-1 = bytes ND-1..0 of P' = round(D/S 2^T) + 2^T with T = 8 ND - 2
+// (ND = 4: 31-bit, K1-TC; ND = 5: 39-bit, K2-TC), col == c is the constant
+// 2^T, col > c zero padding.  One thread writes the 16 bytes of one (chunk, n).
 __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_t row0,
-                               int64_t rows, int64_t n, int c, int BLK, int NB,
+                               int64_t rows, int64_t n, int c, int BLK, int NB, int ND,
                                const double *__restrict__ S, uint8_t *__restrict__ Bpack,
                                int64_t tile0, int64_t tiles) {
+    const int T = 8 * ND - 2;
+    const double scaleT = ldexp(1.0, T);
+    const int64_t offT = 1LL << T;
     const int64_t total = tiles * (BK / 16) * NB;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -81,8 +85,8 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
         const int64_t tt = tile0 + rest / (BK / 16);
         const int bi = nn / BLK, col = nn - bi * BLK;
         uint32_t wv[4] = {0, 0, 0, 0};
-        if (bi < 4 && col <= c) {
-            const int shift = 8 * (3 - bi);
+        if (bi < ND && col <= c) {
+            const int shift = 8 * (ND - 1 - bi);
 #pragma unroll
             for (int p = 0; p < 16; p++) {
                 const int64_t j = tt * BK + kc * 16 + p;       // global point index
@@ -90,10 +94,10 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
                 if (j < n && j >= row0 && j < row0 + rows) {
                     int64_t P;
                     if (col < c) {
-                        double q = D[(j - row0) * ldd + col] / S[col] * 1073741824.0;
-                        P = llrint(q) + 1073741824LL;          // in [0, 2^31]
+                        double q = D[(j - row0) * ldd + col] / S[col] * scaleT;
+                        P = llrint(q) + offT;                  // in [0, 2^(T+1)]
                     } else {
-                        P = 1073741824LL;                      // constant column
+                        P = offT;                              // constant column
                     }
                     byte = (uint32_t)((P >> shift) & 0xFF);
                 }
@@ -113,6 +117,9 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
 // rows of the packed D-slice operand: 4 blocks of BLK = round4(c + 1)
 // columns (matching k1tc2's accumulator blocks)
 int k1tc_bslice_rows(int c) { return 4 * ((c + 1 + 3) & ~3); }
+// ND = 5 (K2-TC): the MMA N = 5 BLK must be a multiple of 16, so BLK = round16(c + 1)
+int tc_bslice_rows(int c, int nd) { return nd == 4 ? k1tc_bslice_rows(c) : nd * ((c + 1 + 15) & ~15); }
+int tc_dslices(const TcOperand &op) { return op.version == 3 ? 5 : 4; }
 
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean) {
     tc::k_col_mean<<<d, 256, 0, ctx->stream>>>(X, n, d, mean);
@@ -138,8 +145,8 @@ void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, in
 
 // Pack local rows [row0, row0 + rows) into Bpack (tiles covering them).
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
-               int64_t n, int c, const double *S, uint8_t *Bpack) {
-    const int NB = k1tc_bslice_rows(c), BLK = NB / 4;
+               int64_t n, int c, const double *S, uint8_t *Bpack, int nd) {
+    const int NB = tc_bslice_rows(c, nd), BLK = NB / nd;
     // the rank holding the last rows also writes the zero padding up to
     // k1tc_pad_rows(n) (the j-tiles read past n); the layout is linear in
     // 16-point chunks, [chunk][NB][16 B], so any tile width reads it
@@ -148,8 +155,8 @@ void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int6
     const int64_t tiles = ceil_div(end, tc::BK) - tile0;
     const int64_t total = tiles * (tc::BK / 16) * NB;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
-    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, BLK, NB, S, Bpack,
-                                                      tile0, tiles);
+    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, BLK, NB, nd, S,
+                                                      Bpack, tile0, tiles);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
 }

@@ -600,13 +600,16 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
 }
 
 size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c) {
-    (void)op;
-    return k1tc2_vpart_elems(n, nloc, c);
+    return op.version == 3 ? k2tc_vpart_elems(n, nloc, c) : k1tc2_vpart_elems(n, nloc, c);
 }
 
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
               cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
+    if (op.version == 3) {
+        BBMM_REQUIRE(mode == 0, "k2tc: stored K has no derivative mode");
+        return k2tc_matmul(ctx, op.Kq, Bp, S, c, n, nloc, s, Vpart, cap, ev0, ev1);
+    }
     return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1,
                         mode);
 }

@@ -1,0 +1,443 @@
+// k2tc.cu -- stored-K kernel-matmul on the int8 tensor cores (K2-TC).
+//
+// The stored variant of the blackbox matmul V = K D (north
+// star item 2: "a stored-K variant for n where K fits in HBM, with vectorised,
+// coalesced streaming of K per iteration"; PAPER.md:706-708 counts one MMM
+// with K per mBCG iteration).  K is materialised ONCE per call, already in the
+// exact fixed-point form of the K1-TC contraction, with one
+// more slice because K is built once (and the fp32 kernel values then keep all
+// their bits):
+//   k~ = K/s in [0, 1]  ->  round(k~ 2^30), four u8 slices q0 (low) .. q3
+// i.e. 4 bytes per entry like fp32, laid out tile by tile exactly as the
+// tcgen05 MMA reads its A operand from shared memory.  (Three slices, i.e.
+// 22-bit k~ as on the fly, measured 1.4e-4 solve error against the oracle at
+// the C2 shape, n = 3000: over the 1e-4 bar where mBCG is not converged.)  Every mBCG
+// iteration then streams the slices from HBM with bulk copies (TMA engine) and
+// contracts them with the packed search directions (k1tc.cu format with five
+// u8 slices p4..p0: D as 39-bit fixed point per column) on the int8 tensor
+// cores with exact uint32 accumulation in TMEM.  The kernel is bound by HBM
+// (4 n_loc n bytes per K D); the tensor work (20 slice products) is < 50 % of
+// the int8 pipe.  Why 39 bits of D (K1-TC uses 31): where mBCG is not yet
+// converged at p the iterates amplify per-iteration rounding of D -- an fp64
+// emulation at the C2 shape (n = 3000, p = 20) moves the solves by 1.3e-4
+// with 31-bit D and by 2.9e-6 with 39-bit D.
+//
+// CTA (persistent, one per SM, 192 threads):
+//   warps 0-3: epilogue -- drain a unit's accumulators (TMEM lane quarter w),
+//              fold the six weighted blocks into fp64, write Vpart
+//   warp 4   : producer -- bulk copies of the K-slice tile (32 KB) and the
+//              D-slice tile (NB x 64 B) of each 64-point stage
+//   warp 5   : MMA issuer -- 4 tcgen05.mma.kind::i8 (q3 .. q0 times the
+//              whole [p4|p3|p2|p1|p0] operand) per 32-point K-step
+// Work unit = (128-row block, j-split); a split never exceeds the uint32
+// accumulation window, so each unit is drained exactly once, into one of two
+// TMEM accumulator sets (the MMAs of unit u+1 overlap the drain of unit u).
+#include <algorithm>
+#include <cmath>
+
+#include "bbmm_internal.cuh"
+#include "k1_kernels.cuh"
+#include "pair_common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace bbmm {
+namespace k2tc {
+
+constexpr int BM = 128;                    // rows per unit (TMEM lanes)
+constexpr int SK = 64;                     // j points per pipeline stage
+constexpr int NQ = 4;                      // K slices (30-bit fixed point)
+constexpr int ND = 5;                      // D slices (39-bit fixed point, k1tc_pack nd = 5)
+constexpr int SLICE_BYTES = BM * SK;       // one u8 slice of a tile: [SK/16][BM][16 B]
+constexpr int A_BYTES = NQ * SLICE_BYTES;  // q0 | q1 | q2 | q3
+// uint32 accumulation bound: block k collects q_a p_b with a + b = 7 - k; all
+// bytes <= 255, q3 <= 0x40, p4 <= 0x80, so the largest per-point block sum is
+// a + b = 3: 64*255 + 3*255*255 = 211395 -> < 20317 points per window.
+constexpr int BLOCK_MAX = 211395;
+constexpr int WINDOW = (int)(4294967295ull / BLOCK_MAX) / SK * SK;
+static_assert((double)WINDOW * BLOCK_MAX < 4294967296.0, "uint32 window bound");
+constexpr int kThreads = 192;
+constexpr int PRODUCER_WARP = 4, MMA_WARP = 5;
+
+constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
+constexpr __host__ __device__ int pow2_cols(int x) {
+    return x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512;
+}
+
+template <int C>
+struct Cfg {
+    static constexpr int C1 = C + 1;            // + constant offset column
+    static_assert(C1 <= 48, "too many columns");
+    static constexpr int BLK = (C1 + 15) & ~15; // N = ND BLK must be a multiple of 16
+    static constexpr int NB = ND * BLK;         // MMA N: [p4 | p3 | p2 | p1 | p0]
+    static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
+    static constexpr int NBLK = NQ + ND - 1;    // accumulator blocks
+    static constexpr int ACC_COLS = NBLK * BLK; // block k has weight 2^(8 (7 - k))
+    static_assert(NBLK == 8, "fold weights below assume 8 blocks");
+    static constexpr int ACC_END = r32(ACC_COLS);
+    static constexpr int NSET = 2 * ACC_END <= 512 ? 2 : 1;
+    static constexpr int TMEM_COLS = pow2_cols(NSET * ACC_END);
+    static constexpr int B_BYTES = NB * SK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES_FIT = (227 * 1024 - 2048) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT < 8 ? STAGES_FIT : 8;
+    static_assert(STAGES >= 3, "shared-memory ring too shallow");
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+};
+
+// --------------------------------------------------------------------------
+// Build: Kq tile (rb, t) = the four u8 slices of round(k~ 2^30) for rows
+// rb*128.. and points t*SK.. (zeros past n_loc / n), K-major core-matrix
+// layout [slice][SK/16 chunks][128 rows][16 B].  Thread = row; kernel values
+// from direct fp32 differences of the scaled inputs (same k~ map as K2).
+// --------------------------------------------------------------------------
+template <int KIND, int D>
+__global__ void __launch_bounds__(BM)
+k_build_kq(const float *__restrict__ Xs, int64_t n, int64_t r0, int64_t nloc, int64_t ntiles,
+           uint8_t *__restrict__ Kq) {
+    constexpr int DS = round4(D);
+    __shared__ float xj_s[SK][DS];
+    const int64_t t = blockIdx.x, rb = blockIdx.y;
+    const int rl = threadIdx.x;
+    const int64_t i = rb * BM + rl;
+    for (int e = threadIdx.x; e < SK * DS; e += BM) {
+        const int jj = e / DS;
+        const int64_t j = t * SK + jj;
+        xj_s[jj][e % DS] = j < n ? Xs[j * DS + e % DS] : 0.0f;
+    }
+    float xi[D];
+    const bool vi = i < nloc;
+#pragma unroll
+    for (int q = 0; q < D; q++) xi[q] = vi ? Xs[(r0 + i) * DS + q] : 0.0f;
+    __syncthreads();
+    uint8_t *tile = Kq + (rb * ntiles + t) * (int64_t)A_BYTES;
+#pragma unroll 1
+    for (int ch = 0; ch < SK / 16; ch++) {
+        uint32_t w[NQ][4];
+#pragma unroll
+        for (int g = 0; g < 4; g++) {
+            uint32_t q[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const int jj = ch * 16 + 4 * g + v;
+                const int64_t j = t * SK + jj;
+                float rs2 = 0.0f;
+#pragma unroll
+                for (int qd = 0; qd < D; qd++) {
+                    const float df = xi[qd] - xj_s[jj][qd];
+                    rs2 = fmaf(df, df, rs2);
+                }
+                // K_ii = s exactly (rs2 = 0 -> k~ = 1 -> q = 2^30); k~ 2^30 keeps every bit
+                // of the fp32 value for k~ >= 2^-6 (and 2^-31 absolute below)
+                const float kv = (vi && j < n) ? kval_scaled<KIND>(r0 + i == j ? 0.0f : rs2) : 0.0f;
+                q[v] = __float2uint_rn(kv * 1073741824.0f);
+            }
+#pragma unroll
+            for (int a = 0; a < NQ; a++) {
+                // byte a of each of the four words, in point order
+                const uint32_t lo = __byte_perm(q[0], q[1], a | ((a + 4) << 4));
+                const uint32_t hi = __byte_perm(q[2], q[3], a | ((a + 4) << 4));
+                w[a][g] = __byte_perm(lo, hi, 0x5410);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < NQ; a++) {
+            uint4 *dst = reinterpret_cast<uint4 *>(tile + a * SLICE_BYTES + (ch * BM + rl) * 16);
+            *dst = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// V (split s of unit u) = s_out * S_c * sum_j k~_ij (P'_jc - 2^38) 2^-68
+// --------------------------------------------------------------------------
+template <int C>
+__global__ void __launch_bounds__(kThreads, 1)
+k2tc_stored(const uint8_t *__restrict__ Kq, const uint8_t *__restrict__ Bpack,
+            const double *__restrict__ Sc, int64_t nloc, int64_t rbs, int64_t ntiles, int sp,
+            int64_t tps, double s, double *__restrict__ Vpart) {
+    using K = Cfg<C>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full_b[K::STAGES], free_b[K::STAGES];
+    __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2], init_done;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t U = rbs * sp;
+
+    if (tid == 0) {
+        for (int q = 0; q < K::STAGES; q++) {
+            ptx::mbar_init(&full_b[q], 1);
+            ptx::mbar_init(&free_b[q], 1);
+        }
+        for (int q = 0; q < 2; q++) {
+            ptx::mbar_init(&acc_full[q], 1);
+            ptx::mbar_init(&acc_empty[q], 4);     // one elected lane per epilogue warp
+        }
+        ptx::mbar_init(&init_done, 4);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<K::TMEM_COLS>(&tmem_base_sh);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == PRODUCER_WARP) {
+        // ------------------------------------------------------------ producer
+        if (ptx::elect_one()) {
+            const uint64_t pol = ptx::policy_evict_first();   // K slices are read once
+            int64_t it = 0;
+            for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+                const int64_t rb = u / sp, t0 = (u % sp) * tps, t1 = min(ntiles, t0 + tps);
+                for (int64_t t = t0; t < t1; t++, it++) {
+                    const int st = (int)(it % K::STAGES);
+                    ptx::mbar_wait(&free_b[st], (uint32_t)(((it / K::STAGES) & 1) ^ 1));
+                    uint8_t *sb = smem + st * K::STAGE_BYTES;
+                    ptx::mbar_arrive_expect_tx(&full_b[st], K::STAGE_BYTES);
+                    ptx::bulk_g2s_hint(sb, Kq + (rb * ntiles + t) * (int64_t)A_BYTES, A_BYTES,
+                                       &full_b[st], pol);
+                    ptx::bulk_g2s(sb + A_BYTES, Bpack + t * (int64_t)K::B_BYTES, K::B_BYTES,
+                                  &full_b[st]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == MMA_WARP) {
+        // --------------------------------------------------------- MMA issuer
+        constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
+        const bool leader = ptx::elect_one();
+        ptx::mbar_wait(&init_done, 0);
+        ptx::tc_fence_after();
+        int64_t it = 0;
+        int uc = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, uc++) {
+            const int64_t t0 = (u % sp) * tps, t1 = min(ntiles, t0 + tps);
+            const int set = uc % K::NSET;
+            if (uc >= K::NSET) ptx::mbar_wait(&acc_empty[set], (uint32_t)(((uc / K::NSET) - 1) & 1));
+            ptx::tc_fence_after();
+            const uint32_t acc = tmem + set * K::ACC_END;
+            for (int64_t t = t0; t < t1; t++, it++) {
+                const int st = (int)(it % K::STAGES);
+                ptx::mbar_wait(&full_b[st], (uint32_t)((it / K::STAGES) & 1));
+                ptx::tc_fence_after();
+                if (leader) {
+                    const uint32_t sa = ptx::smem_u32(smem + st * K::STAGE_BYTES);
+                    const uint32_t sbb = sa + A_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < SK / 32; ks++) {
+                        const uint64_t bd = ptx::smem_desc_kmajor(sbb + ks * 2 * K::NB * 16, K::NB * 16, 128);
+                        const uint32_t ka = sa + ks * 2 * BM * 16;
+                        // q_a (weight 2^(8a)) times [p4|..|p0] -> blocks 3 - a .. 7 - a
+#pragma unroll
+                        for (int a = NQ - 1; a >= 0; a--)
+                            ptx::mma_i8_ss(acc + (NQ - 1 - a) * K::BLK,
+                                           ptx::smem_desc_kmajor(ka + a * SLICE_BYTES, BM * 16, 128),
+                                           bd, IDQ, 1u);
+                    }
+                    ptx::mma_commit(&free_b[st]);
+                }
+                __syncwarp();
+            }
+            if (leader) ptx::mma_commit(&acc_full[set]);
+            __syncwarp();
+        }
+    } else {
+        // ----------------------------------------------------------- epilogue
+        const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+        {
+            constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+            for (int q = 0; q < K::NSET * K::ACC_END; q += 8) ptx::tmem_st8(lane_base + q, z);
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&init_done);
+        }
+        constexpr int CS = (C + 3) & ~3;
+        int uc = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, uc++) {
+            const int64_t rb = u / sp;
+            const int split = (int)(u % sp);
+            const int set = uc % K::NSET;
+            ptx::mbar_wait(&acc_full[set], (uint32_t)((uc / K::NSET) & 1));
+            ptx::tc_fence_after();
+            const uint32_t base = lane_base + set * K::ACC_END;
+            double a[C + 1];
+#pragma unroll
+            for (int c = 0; c <= C; c++) a[c] = 0.0;
+#pragma unroll
+            for (int q0 = 0; q0 < K::ACC_END; q0 += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld32(base + q0, v);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; e++) {
+                    const int col = q0 + e, k = col / K::BLK, c = col % K::BLK;
+                    if (col < K::ACC_COLS && c <= C)
+                        a[c] = fma(0x1p56 / (double)(1ull << (8 * k)), (double)v[e], a[c]);
+                }
+            }
+            // zero the set for its next unit, then hand it back to the issuer
+            {
+                constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int q = 0; q < K::ACC_END; q += 8) ptx::tmem_st8(base + q, z);
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&acc_empty[set]);
+            }
+            const int64_t row = rb * BM + warp * 32 + lane;
+            if (row < nloc) {
+                double *out = Vpart + ((int64_t)split * nloc + row) * CS;
+                const double bs = s * 0x1p-68;
+#pragma unroll
+                for (int c = 0; c < C; c++) out[c] = bs * Sc[c] * (a[c] - a[C]);
+#pragma unroll
+                for (int c = C; c < CS; c++) out[c] = 0.0;
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<K::TMEM_COLS>(tmem);
+    }
+}
+
+struct Plan {
+    int64_t rbs, ntiles, tps;
+    int sp, grid;
+};
+
+// Split the j range so that (a) a split never exceeds the accumulation window
+// and (b) the persistent CTAs get balanced work: minimise the tiles of the
+// busiest CTA, ceil(units / grid) * tiles_per_split (ties: fewer splits).
+static Plan plan(int64_t nloc, int64_t npad) {
+    Plan p;
+    p.rbs = ceil_div(std::max<int64_t>(nloc, 1), BM);
+    p.ntiles = npad / SK;
+    const int64_t sp_min = std::max<int64_t>(1, ceil_div(p.ntiles, WINDOW / SK));
+    int64_t best = -1, best_sp = sp_min;
+    for (int64_t sp = sp_min; sp <= sp_min + 64 && sp <= p.ntiles; sp++) {
+        const int64_t tps = ceil_div(p.ntiles, sp);
+        const int64_t spr = ceil_div(p.ntiles, tps);          // non-empty splits
+        const int64_t U = p.rbs * spr;
+        const int64_t g = std::min<int64_t>(U, kNumSMs);
+        const int64_t cost = ceil_div(U, g) * tps + 2 * ceil_div(U, g);   // + per-unit drain
+        if (best < 0 || cost < best) { best = cost; best_sp = sp; }
+    }
+    p.tps = ceil_div(p.ntiles, best_sp);
+    p.sp = (int)ceil_div(p.ntiles, p.tps);
+    p.grid = (int)std::min<int64_t>(p.rbs * p.sp, kNumSMs);
+    return p;
+}
+
+template <int C>
+static int launch(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const double *S,
+                  int64_t nloc, int64_t npad, double s, double *Vpart, size_t cap) {
+    using K = Cfg<C>;
+    const Plan p = plan(nloc, npad);
+    BBMM_REQUIRE((size_t)p.sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k2tc)");
+    static bool attr = false;
+    if (!attr) {
+        BBMM_CUDA(cudaFuncSetAttribute(k2tc_stored<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       K::SMEM));
+        attr = true;
+    }
+    k2tc_stored<C><<<p.grid, kThreads, K::SMEM, ctx->stream>>>(Kq, Bp, S, nloc, p.rbs, p.ntiles,
+                                                                p.sp, p.tps, s, Vpart);
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+    return p.sp;
+}
+
+}  // namespace k2tc
+
+// ======================================================================
+// host side
+// ======================================================================
+bool k2tc_supported(int c) {
+    switch (c) {
+        case 1: case 2: case 4: case 8: case 11: case 16: case 17: case 32: case 33: return true;
+        default: return false;
+    }
+}
+
+size_t k2tc_vpart_elems(int64_t n, int64_t nloc, int c) {
+    const k2tc::Plan p = k2tc::plan(nloc, k1tc_pad_rows(n));
+    return (size_t)p.sp * std::max<int64_t>(nloc, 1) * ((c + 3) & ~3);
+}
+
+size_t k2tc_kq_bytes(int64_t n, int64_t nloc) {
+    return (size_t)ceil_div(std::max<int64_t>(nloc, 1), k2tc::BM) * k2tc::BM *
+           (size_t)k1tc_pad_rows(n) * k2tc::NQ;
+}
+
+void k2tc_build(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+                int64_t nloc, uint8_t *Kq) {
+    if (nloc <= 0) return;
+    const int64_t npad = k1tc_pad_rows(n);
+    const int64_t ntiles = npad / k2tc::SK;
+    dim3 grid((unsigned)ntiles, (unsigned)ceil_div(nloc, k2tc::BM));
+    if (kind == BBMM_RBF) {
+        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq<0, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
+                                   Xs, n, r0, nloc, ntiles, Kq)))
+    } else {
+        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq<1, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
+                                   Xs, n, r0, nloc, ntiles, Kq)))
+    }
+    BBMM_LAUNCH_CHECK();
+    ctx->launches++;
+}
+
+TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const float *Xs, int dp,
+                           int64_t n, int d, int c, const Hyper &h, int64_t r0, int64_t nloc,
+                           int64_t npad_rows, float **Kst) {
+    *Kst = nullptr;
+    if (!stored) return tc_prepare(ctx, X, n, d, c, h, npad_rows);
+    TcOperand op;
+    if (ctx->matmul_tc && k2tc_supported(c)) {
+        uint8_t *kq = (uint8_t *)ctx->ws.get("Kq", k2tc_kq_bytes(n, nloc));
+        k2tc_build(ctx, h.kind, Xs, dp, n, r0, nloc, kq);
+        op.version = 3;
+        op.d = d;
+        op.Kq = kq;
+        return op;
+    }
+    if (nloc > 0) {
+        const int64_t ldk = ((n + 3) / 4) * 4;
+        *Kst = (float *)ctx->ws.get("Kst", (size_t)nloc * ldk * 4);
+        build_stored_k(ctx, h.kind, Xs, dp, n, r0, nloc, h.s, *Kst);
+    }
+    return op;
+}
+
+int k2tc_matmul(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const double *S, int c,
+                int64_t n, int64_t nloc, double s, double *Vpart, size_t cap, cudaEvent_t ev0,
+                cudaEvent_t ev1) {
+    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    int sp = 1;
+    const int64_t npad = k1tc_pad_rows(n);
+    if (nloc > 0) {
+        switch (c) {
+            case 1: sp = k2tc::launch<1>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 2: sp = k2tc::launch<2>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 4: sp = k2tc::launch<4>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 8: sp = k2tc::launch<8>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 11: sp = k2tc::launch<11>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 16: sp = k2tc::launch<16>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 17: sp = k2tc::launch<17>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 32: sp = k2tc::launch<32>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            case 33: sp = k2tc::launch<33>(ctx, Kq, Bp, S, nloc, npad, s, Vpart, cap); break;
+            default: throw Error{BBMM_ERR_ARG, "k2tc: unsupported column count"};
+        }
+    }
+    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    return sp;
+}
+
+}  // namespace bbmm

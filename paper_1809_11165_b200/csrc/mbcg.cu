@@ -668,9 +668,11 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     size_t vcap = use_sor ? (size_t)std::max<int64_t>(nloc, 1) * cs
                  : use_tc ? tc_vpart_elems(a.tc, a.n, nloc, c) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
     const int64_t npad_tc = use_tc ? k1tc_pad_rows(npad) : 0;
-    uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(c)) : nullptr;
+    const int tc_nd = use_tc ? tc_dslices(a.tc) : 4;
+    const int tc_rows = tc_bslice_rows(c, tc_nd);
+    uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * tc_rows) : nullptr;
     double *Stc = use_tc ? (double *)ws.get("tc_S", kMaxCols * 8) : nullptr;
-    if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, (size_t)npad_tc * k1tc_bslice_rows(c), sm));
+    if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, (size_t)npad_tc * tc_rows, sm));
     double *Vpart = (double *)ws.get("cg_Vpart", std::max<size_t>(vcap, 1) * 8);
     const PassGeom g = pass_geom(nloc, c);
     const int nblk = (int)g.grid.x;
@@ -815,8 +817,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             // tensor-core operand: global column scales, then int8 slices
             k1tc_colmax(ctx, D, c, nloc, c, Stc);
             if (multi) allreduce_max(ctx, Stc, c);
-            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp);
-            if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * k1tc_bslice_rows(c));
+            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp, tc_nd);
+            if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * tc_rows);
         } else if (multi && !use_sor) {          // SoR needs only local rows of D
             allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
         }

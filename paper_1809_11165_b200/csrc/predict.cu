@@ -138,12 +138,8 @@ void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int
     double *ldp = (double *)ws.get("logdet_pre", 8);
     precond_setup(ctx, L, n, k > 0 ? k_used : 0, h.noise_var, cholC, ldp);
     float *Kst = nullptr;
-    if (stored && nloc > 0) {
-        const int64_t ldk = ((n + 3) / 4) * 4;
-        Kst = (float *)ws.get("Kst", (size_t)nloc * ldk * 4);
-        build_stored_k(ctx, h.kind, Xs, dp, n, rr.r0, nloc, h.s, Kst);
-    }
-    TcOperand tcop = Kst ? TcOperand{} : tc_prepare(ctx, X, n, d, CW, h, rr.nb * ctx->nranks);
+    TcOperand tcop = prepare_operator(ctx, stored, X, Xs, dp, n, d, CW, h, rr.r0, nloc,
+                                      rr.nb * ctx->nranks, &Kst);
     MbcgArgs a{Xs, dp, h.kind, h.s, tcop, Kst, n, rr.r0, nloc, rr.nb, h.noise_var, L,
                k > 0 ? k_used : 0, CW, max_iter, tol};
 

@@ -204,6 +204,18 @@ def test_tensor_core_path_is_selected(ctx, orc):
     assert g["stats"]["matmul_path"] == 0
 
 
+def test_stored_tensor_core_path_is_selected(ctx, orc):
+    """BBMM_STORED under the default precision streams K as int8 slices on tcgen05 (path 3);
+    FP64ACC keeps the fp32 stored K (path 1).  Both agree with the oracle."""
+    cfg = synth.scaled(synth.CONFIGS["C1"], 3338)
+    pr, g, o = run_both(ctx, orc, cfg, kmode=bb.STORED)
+    assert g["stats"]["matmul_path"] == 3
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+    pr, g, o = run_both(ctx, orc, cfg, kmode=bb.STORED, prec=bb.FP64ACC)
+    assert g["stats"]["matmul_path"] == 1
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+
+
 def test_tiny_problem(ctx, orc):
     cfg = synth.scaled(synth.CONFIGS["C4"], 7)
     cfg = synth.dataclasses.replace(cfg, k=3, t=2, p=7)
@@ -254,6 +266,24 @@ def test_full_size_matmul_sampled_rows(ctx, orc, name):
     absb = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D), rows=rows)
     err = np.abs(V[rows] - ref)
     assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
+
+
+def test_full_size_stored_matmul_sampled_rows(ctx, orc):
+    """C2 at its BASELINE size (Matern-5/2 ARD, n = 45 730 > one uint32 accumulation window),
+    stored K as int8 slices (the launch configuration of the stored mBCG): sampled rows vs the
+    oracle, held to the matmul bound (fp32 kernel values + 22-bit fixed point)."""
+    cfg = synth.CONFIGS["C2"]
+    pr = synth.make_problem(cfg, seed=0)
+    c = cfg.t + 1
+    D = synth.random_block(cfg.n, c, seed=4).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), bb.STORED).cpu().numpy()
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, cfg.n - 1],
+                                     np.random.default_rng(1).integers(0, cfg.n, 40)]))
+    ref = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D, rows=rows)
+    absb = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D), rows=rows)
+    bound = 2e-6 * absb + 2.0**-22 * math.exp(pr.log_s) * np.abs(D).sum(0) + 1e-12
+    err = np.abs(V[rows] - ref)
+    assert np.all(err <= bound), float((err / bound).max())
 
 
 @pytest.mark.slow
