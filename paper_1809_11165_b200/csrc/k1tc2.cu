@@ -101,17 +101,20 @@ struct Cfg {
     static constexpr int END = BUF_OFF + NBUF * BK;
     static_assert(END <= 512, "TMEM budget exceeded");
     static constexpr int B8_BYTES = NB * BK;                   // int8 D slices per tile
-    static constexpr int XB_BYTES = 3 * DA * BK * 4;           // tf32 B' per tile
-    static constexpr int STAGE_BYTES = B8_BYTES + XB_BYTES;
+    static constexpr int XB_BYTES = 2 * DA * BK * 4;           // tf32 B' per tile: [hi | lo]
     static constexpr int AP_BYTES = BM * 3 * DA * 4;           // row operand A' (smem)
-    // Shared-memory ring of NBUF + 1 .. NBUF + 3 stages (as the budget allows):
-    // the issuer checks stage t + NBUF before it waits for tile t's A slices,
-    // i.e. ring depth - NBUF - 1 tile periods after the stage was released.
     static constexpr int STATIC_BYTES = (C + 1) * BM * 8 + 512;   // acc_sm + barriers
-    static constexpr int STAGES_FIT = (227 * 1024 - STATIC_BYTES - AP_BYTES - 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT < NBUF + 3 ? STAGES_FIT : NBUF + 3;
-    static_assert(STAGES >= NBUF + 1, "shared-memory ring too shallow");
-    static constexpr int RAW = STAGES * STAGE_BYTES + AP_BYTES + 1024;
+    // Two shared-memory rings, each refilled as soon as its consumer MMA completes:
+    // XB (read by the distance MMA of tile t, issued NBUF tiles before tile t's
+    // int8 MMAs) and B8 (read by the int8 MMAs).  Depths as the budget allows.
+    static constexpr int BUDGET = 227 * 1024 - STATIC_BYTES - AP_BYTES - 1024;
+    static constexpr int XS = (3 * XB_BYTES + (NBUF + 3) * B8_BYTES <= BUDGET) ? 3 : 2;
+    static constexpr int QS_FIT = (BUDGET - XS * XB_BYTES) / B8_BYTES;
+    static constexpr int QS = QS_FIT < NBUF + 3 ? QS_FIT : NBUF + 3;
+    static_assert(QS >= 2, "shared-memory ring too shallow");
+    static constexpr int Q_OFF = XS * XB_BYTES;                // B8 ring after the XB ring
+    static constexpr int AP_OFF = Q_OFF + QS * B8_BYTES;       // then the row operand
+    static constexpr int RAW = AP_OFF + AP_BYTES + 1024;
     static_assert(RAW + STATIC_BYTES <= 227 * 1024, "shared memory budget exceeded");
     // >= 120 KB so that a single CTA (which owns all 512 TMEM columns) is resident per SM
     static constexpr int SMEM = RAW > 122880 ? RAW : 122880;
@@ -168,7 +171,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full_b[K::STAGES], free_b[K::STAGES];
+    __shared__ __align__(8) uint64_t full_x[K::XS], free_x[K::XS], full_q[K::QS], free_q[K::QS];
     __shared__ __align__(8) uint64_t s_full[K::NBUF], a_full[K::NBUF];
     __shared__ __align__(8) uint64_t acc_full, acc_empty, init_done;
     __shared__ uint32_t tmem_base_sh;
@@ -181,9 +184,13 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     constexpr int TPW = WINDOW / BK;
 
     if (tid == 0) {
-        for (int q = 0; q < K::STAGES; q++) {
-            ptx::mbar_init(&full_b[q], 1);
-            ptx::mbar_init(&free_b[q], 1);
+        for (int q = 0; q < K::XS; q++) {
+            ptx::mbar_init(&full_x[q], 1);
+            ptx::mbar_init(&free_x[q], 1);
+        }
+        for (int q = 0; q < K::QS; q++) {
+            ptx::mbar_init(&full_q[q], 1);
+            ptx::mbar_init(&free_q[q], 1);
         }
         for (int q = 0; q < K::NBUF; q++) {
             ptx::mbar_init(&s_full[q], 1);
@@ -202,21 +209,31 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------- producer
-        const bool leader = ptx::elect_one();
-        for (int t = 0; t < ntl; t++) {
-            const int st = t % K::STAGES;
-            const uint32_t ph = (uint32_t)((t / K::STAGES) & 1);
-            if (leader) {
-                ptx::mbar_wait(&free_b[st], ph ^ 1);
-                uint8_t *sb = smem + st * K::STAGE_BYTES;
-                const int64_t tg = t0 + t;
-                ptx::mbar_arrive_expect_tx(&full_b[st], K::STAGE_BYTES);
-                ptx::bulk_g2s(sb, Bpack + tg * K::B8_BYTES, K::B8_BYTES, &full_b[st]);
-                ptx::bulk_g2s(sb + K::B8_BYTES, reinterpret_cast<const uint8_t *>(XB) + tg * K::XB_BYTES,
-                              K::XB_BYTES, &full_b[st]);
+        // loads in the order the MMA issuer consumes them: XB of tiles 0..NBUF-1,
+        // then per tile t: B8(t), XB(t + NBUF)
+        if (ptx::elect_one()) {
+            auto load_x = [&](int t) {
+                const int xi = t % K::XS;
+                ptx::mbar_wait(&free_x[xi], (uint32_t)(((t / K::XS) & 1) ^ 1));
+                ptx::mbar_arrive_expect_tx(&full_x[xi], K::XB_BYTES);
+                ptx::bulk_g2s(smem + xi * K::XB_BYTES,
+                              reinterpret_cast<const uint8_t *>(XB) + (t0 + t) * K::XB_BYTES,
+                              K::XB_BYTES, &full_x[xi]);
+            };
+            auto load_q = [&](int t) {
+                const int qi = t % K::QS;
+                ptx::mbar_wait(&free_q[qi], (uint32_t)(((t / K::QS) & 1) ^ 1));
+                ptx::mbar_arrive_expect_tx(&full_q[qi], K::B8_BYTES);
+                ptx::bulk_g2s(smem + K::Q_OFF + qi * K::B8_BYTES, Bpack + (t0 + t) * K::B8_BYTES,
+                              K::B8_BYTES, &full_q[qi]);
+            };
+            for (int t = 0; t < K::NBUF && t < ntl; t++) load_x(t);
+            for (int t = 0; t < ntl; t++) {
+                load_q(t);
+                if (t + K::NBUF < ntl) load_x(t + K::NBUF);
             }
-            __syncwarp();
         }
+        __syncwarp();
     } else if (warp == MMA_WARP) {
         // ------------------------------------------------------ MMA issuer
         // One thread issues both MMA kinds.  tcgen05.mma ops of one thread
@@ -228,43 +245,49 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         ptx::tc_fence_after();
-        auto wait_stage = [&](int t) {
-            ptx::mbar_wait(&full_b[t % K::STAGES], (uint32_t)((t / K::STAGES) & 1));
+        auto wait_x = [&](int t) {
+            ptx::mbar_wait(&full_x[t % K::XS], (uint32_t)((t / K::XS) & 1));
         };
+        // 3xTF32: A' = [hi | hi | lo] (3 DA), B' = [hi | lo] (2 DA): K groups
+        // (A hi, B hi), (A hi, B lo), (A lo, B hi)
         auto issue_dist = [&](int t) {
-            const int st = t % K::STAGES;
+            const int xi = t % K::XS;
             const int b = t % K::NBUF;
             ptx::tc_fence_after();
             if (leader) {
-                const uint32_t xb = ptx::smem_u32(smem + st * K::STAGE_BYTES + K::B8_BYTES);
-                const uint32_t ap = ptx::smem_u32(smem + K::STAGES * K::STAGE_BYTES);
+                const uint32_t xb = ptx::smem_u32(smem + xi * K::XB_BYTES);
+                const uint32_t ap = ptx::smem_u32(smem + K::AP_OFF);
 #pragma unroll
                 for (int ks = 0; ks < 3 * DA / 8; ks++) {
-                    const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
+                    const int g = ks / (DA / 8), kk = ks % (DA / 8);
+                    const int kb = (g == 1 ? DA / 8 : 0) + kk;
+                    const uint64_t bd = ptx::smem_desc_kmajor(xb + kb * 2 * BK * 16, BK * 16, 128);
                     const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
                     ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
                 }
                 ptx::mma_commit(&s_full[b]);
+                ptx::mma_commit(&free_x[xi]);
             }
             __syncwarp();
         };
         for (int t = 0; t < K::NBUF && t < ntl; t++) {
-            wait_stage(t);
+            wait_x(t);
             issue_dist(t);
         }
         for (int t = 0; t < ntl; t++) {
-            const int st = t % K::STAGES;
+            const int qi = t % K::QS;
             const int b = t % K::NBUF;
             const int win = t / TPW;
             const bool first = (t % TPW) == 0;
             // operands of the next distance MMA: normally resident long ago, so
             // this check overlaps the wait for the compute warps below
-            if (t + K::NBUF < ntl) wait_stage(t + K::NBUF);
+            if (t + K::NBUF < ntl) wait_x(t + K::NBUF);
             if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
             ptx::mbar_wait(&a_full[b], (uint32_t)((t / K::NBUF) & 1));
+            ptx::mbar_wait(&full_q[qi], (uint32_t)((t / K::QS) & 1));
             ptx::tc_fence_after();
             if (leader) {
-                const uint32_t b8 = ptx::smem_u32(smem + st * K::STAGE_BYTES);
+                const uint32_t b8 = ptx::smem_u32(smem + K::Q_OFF + qi * K::B8_BYTES);
                 const uint32_t aq = tmem + K::BUF_OFF + b * BK;
 #pragma unroll
                 for (int ks = 0; ks < BK / 32; ks++) {
@@ -273,7 +296,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ, 1u);          // q1
                     ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ, 1u);      // q0
                 }
-                ptx::mma_commit(&free_b[st]);
+                ptx::mma_commit(&free_q[qi]);
                 if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
             }
             __syncwarp();
@@ -289,7 +312,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32), written to
             // shared memory K-major: [3 DA / 4 chunks][128 rows][4 floats]
             const int rl = sub * 32 + lane;
-            float *ap = reinterpret_cast<float *>(smem + K::STAGES * K::STAGE_BYTES);
+            float *ap = reinterpret_cast<float *>(smem + K::AP_OFF);
 #pragma unroll
             for (int q = 0; q < DA; q++) {
                 const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
@@ -426,8 +449,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 // ---------------------------------------------------------- operand prep
 // Per point: xs = (x - mean) scale (fp32), e = -|xs|^2.
 //   Xa[i]  = [2 xs_i (d), e_i, 1, 0..]            (DA floats, row operand)
-//   XB tile tt (BK points): B'_j = [xs_j, 1, e_j, 0..] split [hi | lo | hi]
-//   stored K-major for the MMA: [3 DA / 4 chunks][BK rows][4 floats].
+//   XB tile tt (BK points): B'_j = [xs_j, 1, e_j, 0..] split [hi | lo]
+//   stored K-major for the MMA: [2 DA / 4 chunks][BK rows][4 floats].
 __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad, int d, int DA,
                            const float *__restrict__ scale, const double *__restrict__ mean,
                            float *__restrict__ Xa, float *__restrict__ XB,
@@ -455,10 +478,10 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
             const float bl = b - bh;
             const int64_t tt = j / BK;
             const int jj = s_col_of((int)(j - tt * BK));
-            float *tile = XB + tt * (int64_t)(3 * DA * BK);
-            const float parts[3] = {bh, bl, bh};
-            for (int pt = 0; pt < 3; pt++) {
-                const int k = pt * DA + q;             // K index in [0, 3 DA)
+            float *tile = XB + tt * (int64_t)(2 * DA * BK);
+            const float parts[2] = {bh, bl};
+            for (int pt = 0; pt < 2; pt++) {
+                const int k = pt * DA + q;             // K index in [0, 2 DA)
                 tile[(k >> 2) * (BK * 4) + jj * 4 + (k & 3)] = parts[pt];
             }
         }
@@ -476,14 +499,14 @@ bool k1tc2_supported(int kind, int d, int c) {
     if (kind != BBMM_RBF) return false;
     const int da = tc2_da(d);
     switch (c) {
-        case 1: case 2: case 4: case 8: case 11: return da <= 24;
-        case 17: return da <= 16;
+        case 1: case 2: case 4: case 8: return da <= 24;
+        case 11: case 17: case 33: return da <= 32;
         default: return false;
     }
 }
 
 int64_t k1tc2_xa_floats(int64_t npad, int d) { return npad * tc2_da(d); }
-int64_t k1tc2_xb_floats(int64_t npad, int d) { return npad * 3 * tc2_da(d); }
+int64_t k1tc2_xb_floats(int64_t npad, int d) { return npad * 2 * tc2_da(d); }
 
 float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h,
                         float *Xa, float *XB, int64_t npad) {
@@ -542,7 +565,9 @@ size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c) {
 }
 
 bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c) {
-    return n_ls == 1 && (c == 11 || c == 17) && k1tc2_supported(kind, d, c);
+    // the instantiated derivative shapes (k1tc2_matmul, mode 1)
+    const int da = tc2_da(d);
+    return n_ls == 1 && kind == BBMM_RBF && ((c == 11 && da <= 24) || (c == 17 && da == 8));
 }
 
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
@@ -569,7 +594,8 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
         BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)
         BBMM_TC2(11, 16) BBMM_TC2(17, 16) BBMM_TC2(1, 24) BBMM_TC2(2, 24) BBMM_TC2(4, 24)
-        BBMM_TC2(8, 24) BBMM_TC2(11, 24)
+        BBMM_TC2(8, 24) BBMM_TC2(11, 24) BBMM_TC2(17, 24) BBMM_TC2(11, 32) BBMM_TC2(17, 32)
+        BBMM_TC2(33, 8) BBMM_TC2(33, 16) BBMM_TC2(33, 24) BBMM_TC2(33, 32)
         throw Error{BBMM_ERR_ARG, "k1tc2: unsupported (c, d)"};
     }
 #undef BBMM_TC2

@@ -199,6 +199,10 @@ def test_tensor_core_path_is_selected(ctx, orc):
     cfg0 = synth.scaled(synth.CONFIGS["C0"], 256)       # max|xs|^2 > 16 -> guard
     pr, g, o = run_both(ctx, orc, cfg0)
     assert g["stats"]["matmul_path"] == 0
+    cfg3 = synth.scaled(synth.CONFIGS["C3"], 2000)      # RBF ARD, d = 26, t + 1 = 33
+    pr, g, o = run_both(ctx, orc, cfg3)
+    assert g["stats"]["matmul_path"] == 2
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
     cfg2 = synth.scaled(synth.CONFIGS["C2"], 500)       # Matern -> CUDA-core path
     pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
     assert g["stats"]["matmul_path"] == 0
