@@ -55,12 +55,15 @@ __global__ void k_colmax_part(const double *__restrict__ D, int64_t ldd, int64_t
         part[(int64_t)blockIdx.x * c + col] = m;
     }
 }
+// one warp per column (max is order-independent)
 __global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c, double *__restrict__ S) {
-    const int col = threadIdx.x;
+    const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (col >= c) return;
     double m = 0.0;
-    for (int b = 0; b < nblk; b++) m = fmax(m, part[(int64_t)b * c + col]);
-    S[col] = m > 0.0 ? m : 1.0;
+    for (int b = lane; b < nblk; b += 32) m = fmax(m, part[(int64_t)b * c + col]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) S[col] = m > 0.0 ? m : 1.0;
 }
 
 // Pack rows [row0, row0 + rows) of D (fp64) into the K-major slice layout
@@ -138,7 +141,7 @@ void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, in
     int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, rb), 2 * kNumSMs));
     double *part = (double *)ctx->ws.get("tc_cmax", (size_t)nblk * c * 8);
     tc::k_colmax_part<<<nblk, dim3(cw, rb), 0, ctx->stream>>>(D, ldd, rows, c, part);
-    tc::k_colmax_final<<<1, 64, 0, ctx->stream>>>(part, nblk, c, S);
+    tc::k_colmax_final<<<(int)ceil_div(c, 8), 256, 0, ctx->stream>>>(part, nblk, c, S);
     BBMM_LAUNCH_CHECK();
     ctx->launches += 2;
 }

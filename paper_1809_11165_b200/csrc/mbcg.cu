@@ -57,13 +57,23 @@ __device__ void block_reduce_cols(double v, double *part, int m, int col_offset)
 }
 
 // --------------------------------------------------------------- kernels
+// red[e] = sum_b part[b][e]: one warp per output, lane l sums b = l, l + 32, ..
+// in order, then a fixed xor-butterfly (every lane ends with the same value):
+// deterministic, and ~nblk/32 dependent loads instead of nblk.
 __global__ void k_reduce_blocks(const double *__restrict__ part, int nblk, int m,
                                 double *__restrict__ red) {
-    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < m; e += blockDim.x * gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m;
+         e += (gridDim.x * blockDim.x) >> 5) {
         double s = 0.0;
-        for (int b = 0; b < nblk; b++) s += part[(int64_t)b * m + e];   // fixed order
-        red[e] = s;
+        for (int b = lane; b < nblk; b += 32) s += part[(int64_t)b * m + e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[e] = s;
     }
+}
+inline int reduce_grid(int m) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 8), 8 * kNumSMs));
 }
 
 // R = B, U = 0, D = 0 ; partial sum of B^2 per column.
@@ -591,8 +601,7 @@ __global__ void k_probes(const int8_t *__restrict__ eps, uint64_t seed, int64_t 
 // host side
 // ======================================================================
 void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red) {
-    k_reduce_blocks<<<std::max(1, (int)ceil_div(m, 256)), 256, 0, ctx->stream>>>(part, nblk, m,
-                                                                                red);
+    k_reduce_blocks<<<reduce_grid(m), 256, 0, ctx->stream>>>(part, nblk, m, red);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
 }
@@ -617,7 +626,7 @@ void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double no
     if (nl > 0) {
         auto f = kpt <= 2 ? k_LtL2<2> : kpt <= 4 ? k_LtL2<4> : kpt <= 6 ? k_LtL2<6> : k_LtL2<8>;
         f<<<nblk, 256, smem, ctx->stream>>>(L, n, rr.r0, nl, k, rpb, part);
-        k_reduce_blocks<<<ceil_div(k * k, 256), 256, 0, ctx->stream>>>(part, nblk, k * k, red);
+        k_reduce_blocks<<<reduce_grid(k * k), 256, 0, ctx->stream>>>(part, nblk, k * k, red);
     } else {
         BBMM_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * k * k, ctx->stream));
     }
@@ -696,11 +705,12 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     int launches = 0;
 
     auto reduce = [&](int m, double *dst) {
-        k_reduce_blocks<<<std::max(1, (int)ceil_div(m, 256)), 256, 0, sm>>>(part, nblk, m, dst);
+        k_reduce_blocks<<<reduce_grid(m), 256, 0, sm>>>(part, nblk, m, dst);
         launches++;
     };
     // W = L^T R (+ |R|^2 already in red[0..c) when with_rr) -> red[c..c+kc)
-    const int ltr_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, kLtrRows),
+    // >= one block per 64 rows so that small problems are not latency-bound on a few blocks
+    const int ltr_blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 64),
                                                                         2 * kNumSMs));
     const size_t smem_ltr = ((size_t)kLtrRows * c + (size_t)kk * c) * 8;
     auto ltr_kernel = c <= 8 ? k_LtR<8> : (c <= 17 ? k_LtR<17> : (c <= 33 ? k_LtR<33> : k_LtR<kMaxCols>));
@@ -735,8 +745,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     auto LtR = [&](double *dst) {
         if (k == 0) return;
         launch_ltr(a.L, k, R, part_ltr, smem_ltr);
-        k_reduce_blocks<<<std::max(1, (int)ceil_div(k * c, 256)), 256, 0, sm>>>(
-            part_ltr, ltr_blocks, k * c, dst);
+        k_reduce_blocks<<<reduce_grid(k * c), 256, 0, sm>>>(part_ltr, ltr_blocks, k * c, dst);
         launches += 2;
     };
     // SoR operator (row f4): T = Bs[:, local] D (the L^T R kernel with L = Bs), all-reduced,
@@ -760,8 +769,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         if (e0) BBMM_CUDA(cudaEventRecord(e0, sm));
         if (nloc > 0) {
             launch_ltr(a.sor_B, msor, D, part_sor, smem_sor);
-            k_reduce_blocks<<<std::max(1, (int)ceil_div(msor * c, 256)), 256, 0, sm>>>(
-                part_sor, ltr_blocks, msor * c, Tsor);
+            k_reduce_blocks<<<reduce_grid(msor * c), 256, 0, sm>>>(part_sor, ltr_blocks, msor * c,
+                                                                    Tsor);
             launches += 2;
         } else {
             BBMM_CUDA(cudaMemsetAsync(Tsor, 0, (size_t)msor * c * 8, sm));

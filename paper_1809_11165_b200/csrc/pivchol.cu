@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cstdint>
+
 #include "bbmm_internal.cuh"
 
 namespace bbmm {
@@ -98,10 +100,20 @@ __global__ void k_piv_init(double *__restrict__ diag, int64_t n, double s, doubl
 // Finish the argmax over block partials; decide pivot m (or stop).
 __global__ void k_piv_select(PivState *st, const double *__restrict__ pv,
                              const int64_t *__restrict__ pi, int nblk, int m, double stop_tol) {
-    if (threadIdx.x != 0 || st->stop) return;
-    double bv = pv[0];
-    int64_t bi = pi[0];
-    for (int b = 1; b < nblk; b++) argmax_combine(bv, bi, pv[b], pi[b]);
+    // one warp: (value, -index) is a total order, so the strided lane partials and the
+    // butterfly give exactly the sequential argmax (ties -> lowest index)
+    if (st->stop) return;
+    const int lane = threadIdx.x;
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int b = lane; b < nblk; b += 32) argmax_combine(bv, bi, pv[b], pi[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        argmax_combine(bv, bi, v2, i2);
+    }
+    if (lane != 0) return;
     if (!(bv > stop_tol)) {
         st->stop = 1;
         st->k_used = m;

@@ -12,7 +12,8 @@ pr = synth.make_problem(cfg, seed=0)
 ctx = bb.Context(0)
 X = torch.from_numpy(pr.X).cuda(); y = torch.from_numpy(pr.y).cuda()
 h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
-kw = dict(t=cfg.t, k=cfg.k, max_iter=cfg.p, tol=0.0, seed=1)
+kw = dict(t=cfg.t, k=cfg.k, max_iter=cfg.p, tol=0.0, seed=1,
+          kmode=bb.STORED if cfg.stored else bb.ONTHEFLY)
 r = bb.mll_and_grad(ctx, X, y, h, **kw)          # warm-up
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity
