@@ -165,6 +165,8 @@ struct TcOperand {
     const float *Xa = nullptr;  // v2 row operand
     const float *XB = nullptr;  // v2 distance tiles
     const uint8_t *Kq = nullptr;  // v3 stored K slices (this rank's rows)
+    int kind = 0;               // kernel family of the operand
+    int nd = 4;                 // D slices of the packed operand (k1tc_pack nd)
 };
 int tc_dslices(const TcOperand &op);   // D slices of the operand's packed format (4 or 5)
 // Prepare the tensor-core inputs for (kind, d, c) if the INT8EXACT mode applies.

@@ -122,7 +122,7 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
 int k1tc_bslice_rows(int c) { return 4 * ((c + 1 + 3) & ~3); }
 // ND = 5 (K2-TC): the MMA N = 5 BLK must be a multiple of 16, so BLK = round16(c + 1)
 int tc_bslice_rows(int c, int nd) { return nd == 4 ? k1tc_bslice_rows(c) : nd * ((c + 1 + 15) & ~15); }
-int tc_dslices(const TcOperand &op) { return op.version == 3 ? 5 : 4; }
+int tc_dslices(const TcOperand &op) { return op.nd; }
 
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean) {
     tc::k_col_mean<<<d, 256, 0, ctx->stream>>>(X, n, d, mean);

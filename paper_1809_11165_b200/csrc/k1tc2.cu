@@ -84,14 +84,19 @@ constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
 // product of weight 2^(8 (5 - k)) (q_a p_b with a + b = 5 - k): all twelve
 // slice products, no truncation, in 6 BLK TMEM columns.  The MMAs always
 // accumulate; the draining warps zero the columns they read.
-template <int C, int DA>
+// ND = number of D slices: 4 (31-bit D, RBF) or 5 (39-bit D, Matern, whose
+// C2 shape is not converged at p: DESIGN.md §6 / reading R29); with 5 slices
+// the MMA N = 5 BLK must be a multiple of 16.
+template <int C, int DA, int ND = 4>
 struct Cfg {
     static constexpr int C1 = C + 1;
     static_assert(C1 <= 48, "too many columns");
-    static constexpr int BLK = (C1 + 3) & ~3;
-    static constexpr int NB = 4 * BLK;                         // D-slice rows (MMA N)
+    static_assert(ND == 4 || ND == 5, "D slices");
+    static constexpr int BLK = ND == 4 ? (C1 + 3) & ~3 : (C1 + 15) & ~15;
+    static constexpr int NB = ND * BLK;                        // D-slice rows (MMA N)
     static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
-    static constexpr int ACC_COLS = 6 * BLK;
+    static constexpr int NBLK = ND + 2;                        // accumulator blocks
+    static constexpr int ACC_COLS = NBLK * BLK;
     static constexpr int ACC_END = r32(ACC_COLS);
     static constexpr int NBUF_FIT = (512 - ACC_END) / BK;
     static constexpr int NBUF = NBUF_FIT < 4 ? NBUF_FIT : 4;     // S/A TMEM buffers
@@ -127,15 +132,17 @@ struct Cfg {
 // cc % NPS == h (so no two warps touch one acc_sm entry) and zeroes the
 // 32-column chunks q with q % NPS == h for the next window (caller waits for
 // the stores).
-template <int C, int BLK, int ACC_END>
+template <int C, int BLK, int ACC_END, int ND>
 __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl, int h) {
+    constexpr int NBLK = ND + 2;
+    constexpr double W0 = ND == 4 ? 0x1p40 : 0x1p48;    // weight of block 0: 2^(8 (ND + 1))
     constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     constexpr int M = (C + NPS) / NPS;             // columns cc = h + NPS m <= C per warp
-    uint32_t v[M][6];
+    uint32_t v[M][NBLK];
 #pragma unroll
     for (int m = 0; m < M; m++)
 #pragma unroll
-        for (int k = 0; k < 6; k++)
+        for (int k = 0; k < NBLK; k++)
             v[m][k] = (h + NPS * m <= C) ? ptx::tmem_ld1(lane_base + k * BLK + h + NPS * m) : 0u;
     ptx::tmem_ld_wait();
 #pragma unroll
@@ -144,7 +151,7 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[B
         if (cc <= C) {
             double a = acc_sm[cc][rl];
 #pragma unroll
-            for (int k = 0; k < 6; k++) a = fma(0x1p40 / (double)(1ull << (8 * k)), (double)v[m][k], a);
+            for (int k = 0; k < NBLK; k++) a = fma(W0 / (double)(1ull << (8 * k)), (double)v[m][k], a);
             acc_sm[cc][rl] = a;
         }
     }
@@ -160,14 +167,17 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[B
 }
 
 // MODE 0: value k~ = K/s (the blackbox matmul);  MODE 1: value k~ r^2
-// (= (dK/dlog l)/s for the isotropic RBF, used by the derivative pass).
+// (= (dK/dlog l)/s for the isotropic RBF, used by the derivative pass);
+// MODE 2: Matern-5/2 k~ = (1 + rh + rh^2/3) e^{-rh}, rh = sqrt(-S) (inputs
+// scaled by sqrt5/l; two MUFU ops per pair: sqrt, ex2), 39-bit D (ND = 5).
 template <int C, int DA, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
           const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
           int64_t nloc, int64_t tiles_per_split, int64_t ntiles, double s,
           double *__restrict__ Vpart) {
-    using K = Cfg<C, DA>;
+    constexpr int ND = MODE == 2 ? 5 : 4;
+    using K = Cfg<C, DA, ND>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -353,7 +363,16 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float sj = __uint_as_float(sv[4 * u + v]);
-                float kv = ex2_approx(sj);
+                float kv;
+                if (MODE == 2) {
+                    // S = -rh^2 (clamped at 0 near the diagonal)
+                    const float rs2 = fmaxf(-sj, 0.0f);
+                    const float rh = sqrt_approx(rs2);
+                    kv = fmaf(rs2, 0.33333333333333333f, rh + 1.0f) *
+                         ex2_approx(-1.4426950408889634f * rh);
+                } else {
+                    kv = ex2_approx(sj);
+                }
                 // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
                 // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
                 if (MODE == 1) kv *= fmaxf(-1.3862943611198906f * sj, 0.0f);
@@ -380,7 +399,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             if (last_of_window) {
                 ptx::mbar_wait_a(a_accf, (uint32_t)(win & 1));
                 ptx::tc_fence_after();
-                drain_window<C, K::BLK, K::ACC_END>(lane_base, acc_sm, sub * 32 + lane, h);
+                drain_window<C, K::BLK, K::ACC_END, ND>(lane_base, acc_sm, sub * 32 + lane, h);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -430,7 +449,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
             double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * CS;
-            const double base = s * 0x1p-52;
+            const double base = s * (ND == 4 ? 0x1p-52 : 0x1p-60);
             const double cacc = acc_sm[C][rl];
 #pragma unroll
             for (int c = 0; c < C; c++) out[c] = base * Sc[c] * (acc_sm[c][rl] - cacc);
@@ -496,8 +515,9 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
 static int tc2_da(int d) { return ((d + 2 + 7) / 8) * 8; }
 
 bool k1tc2_supported(int kind, int d, int c) {
-    if (kind != BBMM_RBF) return false;
     const int da = tc2_da(d);
+    if (kind == BBMM_MATERN52) return (c == 17 || c == 11) && da <= 16;   // MODE 2 instantiations
+    if (kind != BBMM_RBF) return false;
     switch (c) {
         case 1: case 2: case 4: case 8: return da <= 24;
         case 11: case 17: case 33: return da <= 32;
@@ -513,7 +533,8 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
     double *mean = (double *)ctx->ws.get("tc_mean", kMaxDim * 8);
     float *sc_d = (float *)ctx->ws.get("tc_scale", kMaxDim * 4);
     float sc[kMaxDim];
-    const double base = std::sqrt(0.5 / std::log(2.0));
+    // RBF: S = -|xs_i - xs_j|^2 = -(log2 e / 2) r^2 -> k~ = 2^S;  Matern: S = -5 r^2 = -rh^2
+    const double base = h.kind == BBMM_RBF ? std::sqrt(0.5 / std::log(2.0)) : std::sqrt(5.0);
     for (int q = 0; q < d; q++) sc[q] = (float)(base / h.ls[h.n_ls == 1 ? 0 : q]);
     BBMM_CUDA(cudaMemcpyAsync(sc_d, sc, sizeof(float) * d, cudaMemcpyHostToDevice, ctx->stream));
     k1tc_col_mean(ctx, X, n, d, mean);
@@ -536,7 +557,7 @@ template <int C, int DA, int MODE>
 static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                       const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
                       double *Vpart, size_t cap) {
-    using K = tc2::Cfg<C, DA>;
+    using K = tc2::Cfg<C, DA, MODE == 2 ? 5 : 4>;
     const int64_t ntiles = ceil_div(n, tc2::BK);
     const int64_t rb = ceil_div(nloc, tc2::BM);
     int64_t sp = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, rb), ntiles));
@@ -588,6 +609,17 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
         return sp;
     }
+    if (mode == 2) {   // Matern-5/2
+        if (nloc > 0) {
+            if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported Matern shape"};
+        }
+        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        return sp;
+    }
 #define BBMM_TC2(CC, DD) \
     if (c == CC && da == DD) sp = launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
     if (nloc > 0) {
@@ -619,6 +651,8 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         // the direct-difference FP64ACC path.
         if (!(max_sq <= 16.0f)) return op;
         op.version = 2;
+        op.kind = h.kind;
+        op.nd = h.kind == BBMM_MATERN52 ? 5 : 4;
         op.Xa = xa;
         op.XB = xb;
     }
@@ -635,6 +669,10 @@ int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const dou
     if (op.version == 3) {
         BBMM_REQUIRE(mode == 0, "k2tc: stored K has no derivative mode");
         return k2tc_matmul(ctx, op.Kq, Bp, S, c, n, nloc, s, Vpart, cap, ev0, ev1);
+    }
+    if (op.kind == BBMM_MATERN52) {
+        BBMM_REQUIRE(mode == 0, "k1tc2: no Matern derivative mode");
+        mode = 2;
     }
     return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1,
                         mode);

@@ -405,6 +405,8 @@ TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const f
         k2tc_build(ctx, h.kind, Xs, dp, n, r0, nloc, kq);
         op.version = 3;
         op.d = d;
+        op.kind = h.kind;
+        op.nd = k2tc::ND;
         op.Kq = kq;
         return op;
     }

@@ -203,9 +203,12 @@ def test_tensor_core_path_is_selected(ctx, orc):
     pr, g, o = run_both(ctx, orc, cfg3)
     assert g["stats"]["matmul_path"] == 2
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
-    cfg2 = synth.scaled(synth.CONFIGS["C2"], 500)       # Matern -> CUDA-core path
+    cfg2 = synth.scaled(synth.CONFIGS["C2"], 2500)      # Matern-5/2 ARD on the fly (MODE 2)
     pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
-    assert g["stats"]["matmul_path"] == 0
+    assert g["stats"]["matmul_path"] == 2
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
 
 
 def test_stored_tensor_core_path_is_selected(ctx, orc):
