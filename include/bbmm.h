@@ -137,6 +137,19 @@ const char *bbmm_version(void);
 bbmm_status_t bbmm_nccl_unique_id(void *out_128_bytes);
 bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank,
                                 const void *nccl_unique_id_128_bytes);
+/* In-process rank group (SURVEY.md §8e row partition without NCCL): nranks
+ * contexts in ONE process, each driven by its own host thread, may share one
+ * GPU.  Collectives are synchronous and host-staged (each rank synchronises its
+ * stream; sums in rank order, so every rank gets identical bits); a rank that
+ * waits more than 120 s for its peers fails with BBMM_ERR_NCCL.  For testing the
+ * multi-rank data flow on one GPU -- not a performance path.  The group is owned
+ * by the caller and must outlive the contexts that use it.  BBMM_ERR_ARG for
+ * nranks < 1, rank outside [0, nranks) or NULL arguments. */
+typedef struct bbmm_local_group_s *bbmm_local_group_t;
+bbmm_status_t bbmm_local_group_create(int32_t nranks, bbmm_local_group_t *out);
+bbmm_status_t bbmm_local_group_destroy(bbmm_local_group_t group);
+bbmm_status_t bbmm_ctx_set_local_comm(bbmm_ctx_t ctx, bbmm_local_group_t group,
+                                      int32_t rank);
 /* Select the matmul arithmetic for subsequent calls on ctx (default INT8EXACT). */
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p);
 /* Row partition of the multi-GPU path: rank owns

@@ -87,7 +87,11 @@ _lib.bbmm_train_adam.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i3
                                  _i32, _d, _d, _d, _d, _p, _p]
 _lib.bbmm_sor_mbcg.argtypes = [_p, _p, _i64, _i32, _p, _i32, _HP, _i32, _p, _i32, _i64, _i32, _d,
                                _p, _i64, _p, _p, _p, _p]
-for _f in ("bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
+_lib.bbmm_local_group_create.argtypes = [_i32, C.POINTER(_p)]
+_lib.bbmm_local_group_destroy.argtypes = [_p]
+_lib.bbmm_ctx_set_local_comm.argtypes = [_p, _p, _i32]
+for _f in ("bbmm_local_group_create", "bbmm_local_group_destroy", "bbmm_ctx_set_local_comm",
+           "bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
            "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
            "bbmm_mll_and_grad", "bbmm_predict", "bbmm_train_adam", "bbmm_sor_mbcg"):
     getattr(_lib, _f).restype = C.c_int
@@ -182,6 +186,13 @@ class Context:
         self.nranks, self.rank = ws, rk
         return self
 
+    def set_local_comm(self, group: "LocalGroup", rank: int):
+        """Join an in-process rank group (bbmm_ctx_set_local_comm): this context becomes
+        rank `rank`; drive each rank's calls from its own thread."""
+        self.check(_lib.bbmm_ctx_set_local_comm(self._h, group._h, int(rank)))
+        self.nranks, self.rank = group.nranks, int(rank)
+        return self
+
     def set_matmul_precision(self, prec: int):
         self.check(_lib.bbmm_ctx_set_matmul_precision(self._h, int(prec)))
         return self
@@ -190,6 +201,23 @@ class Context:
         r0, r1 = _i64(), _i64()
         self.check(_lib.bbmm_local_rows(self._h, int(n), C.byref(r0), C.byref(r1)))
         return r0.value, r1.value
+
+
+class LocalGroup:
+    """In-process rank group (include/bbmm.h bbmm_local_group_create): the row-partitioned
+    multi-rank path with host-staged collectives, e.g. several contexts on one GPU."""
+
+    def __init__(self, nranks: int):
+        h = _p()
+        st = _lib.bbmm_local_group_create(int(nranks), C.byref(h))
+        if st != 0:
+            raise BBMMError(st, "local_group_create")
+        self._h, self.nranks = h, int(nranks)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.bbmm_local_group_destroy(self._h)
+            self._h = None
 
 
 def _dev(t, dtype, name, ctx):

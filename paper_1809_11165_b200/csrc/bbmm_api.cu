@@ -70,16 +70,19 @@ Hyper make_hyper(const bbmm_hyper_t *hp, int d) {
 // ------------------------------------------------------------------ comm
 void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count) {
     if (ctx->nranks <= 1) return;
+    if (ctx->local) return local_allreduce_sum(ctx, buf, count);
     BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 
 void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count) {
     if (ctx->nranks <= 1) return;
+    if (ctx->local) return local_allreduce_max(ctx, buf, count);
     BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream));
 }
 
 void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank) {
     if (ctx->nranks <= 1) return;
+    if (ctx->local) return local_allgather(ctx, buf, bytes_per_rank);
     char *b = (char *)buf;
     BBMM_NCCL(ncclAllGather(b + (size_t)ctx->rank * bytes_per_rank, b, bytes_per_rank, ncclChar,
                             ctx->comm, ctx->stream));
@@ -345,6 +348,7 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
             ncclCommDestroy(ctx->comm);
             ctx->comm = nullptr;
         }
+        ctx->local = nullptr;
         ctx->nranks = nranks;
         ctx->rank = rank;
         if (nranks > 1) {

@@ -89,6 +89,13 @@ struct MbcgState {
 
 }  // namespace bbmm
 
+namespace bbmm {
+struct LocalGroup;
+void local_allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count);
+void local_allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count);
+void local_allgather(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank);
+}  // namespace bbmm
+
 struct bbmm_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -101,6 +108,7 @@ struct bbmm_ctx_s {
     bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
     int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
+    bbmm::LocalGroup *local = nullptr;   // in-process rank group (comm_local.cu) instead of NCCL
 };
 
 namespace bbmm {

@@ -1,0 +1,152 @@
+"""Multi-rank row partition on ONE GPU.
+
+G contexts on cuda:0, each driven by its own thread, joined in an in-process rank group
+(bbmm_local_group_create / bbmm_ctx_set_local_comm: host-staged all-gather / all-reduce in
+rank order).  Every rank runs the same library code as an NCCL rank -- its row range of K-hat,
+U, R, Z, D, V, the all-gather of the packed search directions and the all-reduces of the dots
+-- so these tests check the partitioned data flow on the real kernels: the G-rank results
+must match the single-rank call (reduction order is the only difference) and the oracle.
+Covers the tensor-core on-the-fly path (RBF and Matern), the stored int8 path, the FP64ACC
+path, ranks with no rows, and the kernel-matmul / mBCG entry points."""
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_1809_11165_b200 as bb  # noqa: E402
+
+
+def dev(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def hyper_of(pr):
+    return bb.Hyper(pr.cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
+
+
+def colwise_rel(a, b):
+    return np.linalg.norm(a - b, axis=0) / np.maximum(np.linalg.norm(b, axis=0), 1e-300)
+
+
+def run_ranks(nranks, fn, prec=bb.INT8EXACT):
+    """fn(ctx) on every rank of an in-process group, one thread per rank; results by rank."""
+    group = bb.LocalGroup(nranks)
+    ctxs = [bb.Context(0, stream=torch.cuda.Stream()) for _ in range(nranks)]
+    for r, c in enumerate(ctxs):
+        c.set_local_comm(group, r).set_matmul_precision(prec)
+    torch.cuda.synchronize()
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            out[r] = fn(ctxs[r])
+        except Exception as e:          # noqa: BLE001  (re-raised below)
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for c in ctxs:
+        c.close()
+    group.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def single(fn, prec=bb.INT8EXACT):
+    ctx = bb.Context(0).set_matmul_precision(prec)
+    try:
+        return fn(ctx)
+    finally:
+        ctx.close()
+
+
+CASES = [  # name, n, kmode, prec, nranks, expected matmul path
+    ("C4", 3000, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
+    ("C4", 3000, bb.ONTHEFLY, bb.INT8EXACT, 3, 2),
+    ("C1", 3338, bb.STORED, bb.INT8EXACT, 2, 3),
+    ("C2", 2500, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
+    ("C3", 2000, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
+    ("C4", 3000, bb.ONTHEFLY, bb.FP64ACC, 2, 0),
+    ("C4", 300, bb.ONTHEFLY, bb.INT8EXACT, 4, 2),     # n = 300, nb = 128: rank 3 owns no rows
+]
+
+
+@pytest.mark.parametrize("name,n,kmode,prec,nranks,path", CASES)
+def test_mll_and_grad_partitioned_matches_single_rank_and_oracle(orc, name, n, kmode, prec,
+                                                                  nranks, path):
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=0)
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        return bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=7, kmode=kmode,
+                               return_solves=True)
+
+    parts = run_ranks(nranks, call, prec)
+    one = single(call, prec)
+    # identical scalars on every rank (rank-ordered reductions)
+    for g in parts[1:]:
+        assert g["mll"] == parts[0]["mll"]
+        np.testing.assert_array_equal(g["grad"], parts[0]["grad"])
+    for r, g in enumerate(parts):
+        assert g["stats"]["matmul_path"] == path
+        r0, r1, _ = bb.row_partition(n, nranks, r)
+        assert g["U"].shape[0] == r1 - r0
+    U = np.concatenate([g["U"].cpu().numpy() for g in parts], 0)
+    g0 = parts[0]
+    # vs the single-rank call: only the reduction order differs
+    assert colwise_rel(U, one["U"].cpu().numpy()).max() < 1e-6
+    assert abs(g0["mll"] - one["mll"]) <= 1e-8 * abs(one["mll"])
+    assert np.linalg.norm(g0["grad"] - one["grad"]) <= 1e-6 * np.linalg.norm(one["grad"])
+    np.testing.assert_array_equal(g0["pivots"], one["pivots"])
+    # vs the oracle at the parity bar
+    o = orc.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, cfg.t, cfg.k,
+                         cfg.p, seed=7)
+    np.testing.assert_array_equal(g0["pivots"], o["pivots"])
+    assert colwise_rel(U, o["U"]).max() < 1e-4
+    assert abs(g0["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g0["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
+
+
+@pytest.mark.parametrize("kmode", [bb.ONTHEFLY, bb.STORED])
+def test_kernel_matmul_partitioned_rows(orc, kmode):
+    cfg = synth.scaled(synth.CONFIGS["C4"], 2500)
+    pr = synth.make_problem(cfg, seed=3)
+    X, h = dev(pr.X), hyper_of(pr)
+    D = dev(synth.random_block(2500, 17, seed=4).astype(np.float64), torch.float64)
+    parts = run_ranks(2, lambda ctx: bb.kernel_matmul(ctx, X, D, h, kmode).cpu().numpy())
+    V = np.concatenate(parts, 0)
+    Vs = single(lambda ctx: bb.kernel_matmul(ctx, X, D, h, kmode).cpu().numpy())
+    np.testing.assert_allclose(V, Vs, rtol=0, atol=1e-12 * np.abs(Vs).max())
+
+
+def test_mbcg_partitioned_rows(orc):
+    cfg = synth.scaled(synth.CONFIGS["C4"], 3000)
+    pr = synth.make_problem(cfg, seed=1)
+    X, h = dev(pr.X), hyper_of(pr)
+    B = synth.random_block(3000, 17, seed=5).astype(np.float64)
+    Lo = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, cfg.k)[0]
+    Ld = dev(Lo.T, torch.float64)
+
+    def call(ctx):
+        r0, r1 = ctx.local_rows(3000)
+        return bb.mbcg(ctx, X, h, dev(B[r0:r1], torch.float64), L=Ld, max_iter=cfg.p)
+
+    parts = run_ranks(2, call)
+    one = single(lambda ctx: bb.mbcg(ctx, X, h, dev(B, torch.float64), L=Ld, max_iter=cfg.p))
+    U = np.concatenate([r["U"].cpu().numpy() for r in parts], 0)
+    assert colwise_rel(U, one["U"].cpu().numpy()).max() < 1e-6
+    np.testing.assert_allclose(parts[0]["alpha"][:5], one["alpha"][:5], rtol=1e-9)
+    np.testing.assert_array_equal(parts[0]["alpha"], parts[1]["alpha"])
