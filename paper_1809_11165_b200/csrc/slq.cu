@@ -1,7 +1,7 @@
 // slq.cu -- Lanczos tridiagonals from the mBCG coefficients (App. A display
 // PAPER.md:468-475, reading R8) and stochastic Lanczos quadrature of
 // log|Phat^{-1} Khat| (Eq. 5-6, runtime PAPER.md:521-528,
-// weights by reading R12).  One thread per probe: builds T_i (size m_i <= p),
+// weights by reading R12).  One block per probe: builds T_i (size m_i <= p),
 // runs an implicit-shift QL eigensolve (Wilkinson shift) tracking only the
 // first row of the eigenvector matrix (all that e_1^T log(T) e_1 needs,
 // PAPER.md:525), then est_i = omega_i sum_j v0_j^2 log(lambda_j).
@@ -41,7 +41,9 @@ __device__ bool tridiag_ql(int m, double *dg, double *e, double *z0) {
             bool early = false;
             for (; i >= l; i--) {
                 double f = s * e[i], b = c * e[i];
-                r = hypot(f, g);
+                // T's entries are O(1/alpha) (no overflow): plain sqrt is enough and has a
+                // much shorter dependency chain than hypot on this latency-bound path
+                r = sqrt(fma(f, f, g * g));
                 e[i + 1] = r;
                 if (r == 0.0) {   // underflow: split and restart
                     dg[i + 1] -= p;
@@ -49,8 +51,9 @@ __device__ bool tridiag_ql(int m, double *dg, double *e, double *z0) {
                     early = true;
                     break;
                 }
-                s = f / r;
-                c = g / r;
+                const double rinv = 1.0 / r;
+                s = f * rinv;
+                c = g * rinv;
                 g = dg[i + 1] - p;
                 r = (dg[i] - g) * s + 2.0 * c * b;
                 p = s * r;
@@ -71,41 +74,40 @@ __device__ bool tridiag_ql(int m, double *dg, double *e, double *z0) {
 }
 
 // ahist/bhist: p x c (row j = iteration j); iters[c]; omega[c] (= rho0).
+// One block per probe (thread 0 works): the QL sweeps of different probes take
+// different paths, so running them as lanes of one warp would serialise them.
 __global__ void k_slq(const double *__restrict__ ahist, const double *__restrict__ bhist,
                       const int *__restrict__ iters, const double *__restrict__ omega, int p,
-                      int c, int col0, int t, double *__restrict__ per_probe,
-                      double *__restrict__ out, int *status) {
-    const int i = threadIdx.x;
-    __shared__ double est_sh[64];
+                      int c, int col0, double *__restrict__ per_probe, int *status) {
+    const int i = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    const int col = col0 + i;
+    const int m = min(iters[col], kMaxP);
+    double dg[kMaxP], e[kMaxP], z0[kMaxP];
+    for (int jj = 0; jj < m; jj++) {
+        double a = ahist[(int64_t)jj * c + col];
+        dg[jj] = 1.0 / a;
+        if (jj > 0) dg[jj] += bhist[(int64_t)(jj - 1) * c + col] / ahist[(int64_t)(jj - 1) * c + col];
+        if (jj < m - 1) e[jj] = sqrt(bhist[(int64_t)jj * c + col]) / a;
+    }
+    if (!tridiag_ql(m, dg, e, z0)) atomicExch(status, (int)BBMM_ERR_NUMERIC);
     double est = 0.0;
-    if (i < t) {
-        const int col = col0 + i;
-        const int m = min(iters[col], kMaxP);
-        double dg[kMaxP], e[kMaxP], z0[kMaxP];
-        for (int jj = 0; jj < m; jj++) {
-            double a = ahist[(int64_t)jj * c + col];
-            dg[jj] = 1.0 / a;
-            if (jj > 0) dg[jj] += bhist[(int64_t)(jj - 1) * c + col] / ahist[(int64_t)(jj - 1) * c + col];
-            if (jj < m - 1) e[jj] = sqrt(bhist[(int64_t)jj * c + col]) / a;
+    for (int jj = 0; jj < m; jj++) {
+        if (!(dg[jj] > 0.0)) {   // Ritz value <= 0: not positive definite
+            atomicExch(status, (int)BBMM_ERR_NUMERIC);
+            continue;
         }
-        if (!tridiag_ql(m, dg, e, z0)) atomicExch(status, (int)BBMM_ERR_NUMERIC);
-        for (int jj = 0; jj < m; jj++) {
-            if (!(dg[jj] > 0.0)) {   // Ritz value <= 0: not positive definite
-                atomicExch(status, (int)BBMM_ERR_NUMERIC);
-                continue;
-            }
-            est += z0[jj] * z0[jj] * log(dg[jj]);
-        }
-        est *= omega[col];
-        if (per_probe) per_probe[i] = est;
+        est += z0[jj] * z0[jj] * log(dg[jj]);
     }
-    if (i < 64) est_sh[i] = (i < t) ? est : 0.0;
-    __syncthreads();
-    if (i == 0) {
-        double s = 0.0;
-        for (int q = 0; q < t; q++) s += est_sh[q];   // fixed order
-        *out = s / (double)t;
-    }
+    per_probe[i] = est * omega[col];
+}
+
+// (1/t) sum of the per-probe estimates, fixed order
+__global__ void k_slq_sum(const double *__restrict__ per_probe, int t, double *__restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int q = 0; q < t; q++) s += per_probe[q];
+    *out = s / (double)t;
 }
 
 }  // namespace
@@ -115,10 +117,11 @@ void slq_logdet(bbmm_ctx_s *ctx, const double *alpha_d, const double *beta_d, co
                 int *status_d) {
     BBMM_REQUIRE(p <= kMaxP, "max_iter too large for the tridiagonal eigensolver (<= 256)");
     BBMM_REQUIRE(t <= 63, "too many probes");
-    k_slq<<<1, 64, 0, ctx->stream>>>(alpha_d, beta_d, iters_d, omega_d, p, c, col0, t, nullptr,
-                                      out_d, status_d);
+    double *pp = (double *)ctx->ws.get("slq_per_probe", 64 * 8);
+    k_slq<<<t, 32, 0, ctx->stream>>>(alpha_d, beta_d, iters_d, omega_d, p, c, col0, pp, status_d);
+    k_slq_sum<<<1, 32, 0, ctx->stream>>>(pp, t, out_d);
     BBMM_LAUNCH_CHECK();
-    ctx->launches++;
+    ctx->launches += 2;
 }
 
 }  // namespace bbmm

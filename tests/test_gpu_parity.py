@@ -269,6 +269,23 @@ def test_errors_are_reported(ctx):
     assert e.value.status == 2
 
 
+def test_stored_k_too_large_is_oom_and_context_survives(ctx, orc):
+    """BBMM_STORED where K does not fit (n = 250 000: 250 GB of int8 slices > HBM) fails with
+    BBMM_ERR_OOM (7) before any launch, and the context keeps working (SURVEY §8b errors)."""
+    n = 250_000
+    cfg = synth.scaled(synth.CONFIGS["C4"], n)
+    pr = synth.make_problem(cfg, seed=0)
+    D = dev(np.ones((n, 2)), torch.float64)
+    with pytest.raises(bb.BBMMError) as e:
+        bb.kernel_matmul(ctx, dev(pr.X), D, hyper_of(pr), bb.STORED)
+    assert e.value.status == 7
+    small = synth.make_problem(synth.scaled(synth.CONFIGS["C4"], 500), seed=0)
+    Ds = synth.random_block(500, 3, seed=1).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(small.X), dev(Ds, torch.float64), hyper_of(small), bb.STORED)
+    ref = orc.kernel_matmul(small.cfg.kind, small.X, small.log_ls, small.log_s, small.log_noise, Ds)
+    assert colwise_rel(V.cpu().numpy(), ref).max() < 2e-5
+
+
 # ---------------------------------------------- full-size sampled parity
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_full_size_matmul_sampled_rows(ctx, orc, name):
