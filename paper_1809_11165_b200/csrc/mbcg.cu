@@ -206,19 +206,36 @@ k_LtR2(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
     }
 }
 
-// S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One block,
-// thread per column: forward then backward substitution.
-__device__ void chol_solve_col(const double *__restrict__ cholC, int k, const double *W, double *S,
-                               int c, int col) {
-    for (int a = 0; a < k; a++) {
-        double s = W[a * c + col];
-        for (int b = 0; b < a; b++) s -= cholC[a * k + b] * S[b * c + col];
-        S[a * c + col] = s / cholC[a * k + a];
-    }
-    for (int a = k - 1; a >= 0; a--) {
-        double s = S[a * c + col];
-        for (int b = a + 1; b < k; b++) s -= cholC[b * k + a] * S[b * c + col];
-        S[a * c + col] = s / cholC[a * k + a];
+// S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One warp per
+// column (warp w takes columns w, w + 32, ..): forward then backward
+// substitution with the column kept in shared memory and each inner product
+// split over the lanes (fixed lane order + xor butterfly: deterministic).
+// Launch: one block of kSolveThreads threads, dynamic smem kSolveThreads/32 * k doubles.
+constexpr int kSolveThreads = 1024;
+__device__ void chol_solve_warps(const double *__restrict__ cholC, int k, const double *W,
+                                 double *__restrict__ S, int c) {
+    extern __shared__ double sol_sh[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *x = sol_sh + (size_t)warp * k;
+    for (int col = warp; col < c; col += (int)(blockDim.x >> 5)) {
+        for (int a = 0; a < k; a++) {
+            double p = 0.0;
+            for (int b = lane; b < a; b += 32) p = fma(cholC[a * k + b], x[b], p);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+            if (lane == 0) x[a] = (W[a * c + col] - p) / cholC[a * k + a];
+            __syncwarp();
+        }
+        for (int a = k - 1; a >= 0; a--) {
+            double p = 0.0;
+            for (int b = a + 1 + lane; b < k; b += 32) p = fma(cholC[b * k + a], x[b], p);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+            if (lane == 0) x[a] = (x[a] - p) / cholC[a * k + a];
+            __syncwarp();
+        }
+        for (int a = lane; a < k; a += 32) S[a * c + col] = x[a];
+        __syncwarp();
     }
 }
 
@@ -393,21 +410,19 @@ __global__ void k_after_B(MbcgState *st, const double *__restrict__ red, const d
                           int k, int c, double tol, double *__restrict__ S,
                           double *__restrict__ rhist) {
     const int col = threadIdx.x;
-    if (col >= c) return;
-    if (st->active[col]) {
+    if (col < c && st->active[col]) {
         double rel = sqrt(red[col]) / st->bnorm[col];
         st->relres[col] = rel;
         rhist[(int64_t)st->j * c + col] = rel;          // relres after iteration j (row f3)
         if (rel < tol) st->active[col] = 0;
     }
-    if (k > 0) chol_solve_col(cholC, k, red + c, S, c, col);
+    if (k > 0) chol_solve_warps(cholC, k, red + c, S, c);
 }
 
 // S = C^{-1} W at initialisation (red = W).
 __global__ void k_solve_S(const double *__restrict__ W, const double *cholC, int k, int c,
                           double *__restrict__ S) {
-    const int col = threadIdx.x;
-    if (col < c && k > 0) chol_solve_col(cholC, k, W, S, c, col);
+    if (k > 0) chol_solve_warps(cholC, k, W, S, c);
 }
 
 // beta = rho'/rho ; record beta_j ; rho = rho' ; exact convergence freezes.
@@ -801,7 +816,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     LtR(red + c);                             // red[c..c+kc) = L^T B
     if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
     if (k > 0) {
-        k_solve_S<<<1, 64, 0, sm>>>(red + c, cholC, k, c, S);
+        k_solve_S<<<1, kSolveThreads, (size_t)(kSolveThreads / 32) * k * 8, sm>>>(red + c, cholC,
+                                                                                k, c, S);
         launches++;
     }
     double *red_rz = red + (size_t)(kk + 1) * c;
@@ -870,7 +886,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         reduce(c, red);
         LtR(red + c);
         if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
-        k_after_B<<<1, 64, 0, sm>>>(st, red, cholC, k, c, a.tol, S, rhist);
+        k_after_B<<<1, kSolveThreads, (size_t)(kSolveThreads / 32) * std::max(k, 1) * 8, sm>>>(
+            st, red, cholC, k, c, a.tol, S, rhist);
         precond_apply(red_rz);
         if (multi) allreduce_sum(ctx, red_rz, c);
         k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
