@@ -353,6 +353,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const uint32_t my_col = lane_base + K::BUF_OFF +
                                 (JW == 32 ? 32 * h : 32 * (h >> 1) + 4 * (h & 1));
         int win = 0;
+        // With only two S/A buffers the MMA side is one tile ahead, so a deferred publish
+        // would sit on the critical path: publish each tile right after its stores then.
+        constexpr bool DEFER = K::NBUF >= 3;
         // Per tile: S = LDTM, A slices = quantise(ex2(S)), STTM over the same
         // columns, arrive a_full.  The TMEM stores land slowly while the int8
         // MMAs of the previous tile stream through TMEM, so the arrive for
@@ -423,7 +426,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];
 #pragma unroll
             for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            if (t > 0) publish(t - 1);
+            if (DEFER && t > 0) publish(t - 1);
             // overwrite own S columns with the A slices q0 | q1 | q2 (column maps
             // above), each half as soon as it is quantised: spreading the stores
             // over the tile measured 3 % faster than one burst at its end
@@ -443,8 +446,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
                 ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
             }
+            if (!DEFER) publish(t);
         }
-        if (ntl > 0) publish(ntl - 1);
+        if (DEFER && ntl > 0) publish(ntl - 1);
         if (h == 0 && valid) {
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
