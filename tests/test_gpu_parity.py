@@ -328,3 +328,37 @@ def test_full_size_pivchol_c4_bit_exact(ctx, orc):
     _, pivo, kuo, reso = orc.pivchol_kernel(cfg.kind, pr.X, pr.log_ls, pr.log_s, cfg.k)
     assert ku == kuo
     np.testing.assert_array_equal(piv, pivo)
+
+
+# ------------------------------------------------ limits and degenerate shapes
+@pytest.mark.parametrize("desc,over", [
+    ("n = 1 (closed form)", dict(n=1, k=1, t=2, p=3)),
+    ("n = 129: one full 128-row tile + 1", dict(n=129, k=7, t=3, p=10)),
+    ("k = 128 (kMaxRank)", dict(n=1500, k=128, t=4, p=10)),
+    ("t = 63 (c = 64 columns, kMaxCols)", dict(n=700, k=10, t=63, p=10)),
+    ("d = 32 (kMaxDim), ARD", dict(n=900, d=32, k=20, t=8, p=15)),
+    ("max_iter = 256 with tol = 0", dict(n=400, k=5, t=3, p=256)),
+])
+def test_limits_and_degenerate_shapes(ctx, orc, desc, over):
+    base = synth.CONFIGS["C3" if "ARD" in desc else "C4"]
+    cfg = synth.dataclasses.replace(base, **over)
+    pr, g, o = run_both(ctx, orc, cfg)
+    np.testing.assert_array_equal(g["pivots"], o["pivots"])
+    assert g["stats"]["k_used"] == o["k_used"]
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4, desc
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"]), desc
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"]), desc
+
+
+@pytest.mark.parametrize("kmode", [bb.ONTHEFLY, bb.STORED])
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 385])
+def test_kernel_matmul_tile_edges(ctx, orc, kmode, n):
+    """Row / point counts around the 128-row tiles and the 384-point operand padding."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], n)
+    pr = synth.make_problem(cfg, seed=5)
+    D = synth.random_block(n, 17, seed=6).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), kmode).cpu().numpy()
+    ref = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
+    err = np.abs(V - ref)
+    bound = matmul_bound(orc, pr, D)
+    assert np.all(err <= bound), float((err / bound).max())
