@@ -244,6 +244,35 @@ void pivchol_sor(bbmm_ctx_s *ctx, const double *Bs, int64_t n, int m, double s, 
 void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
                  const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,
                  int max_iter, double tol, double *mean, double *var);
+// mbcg_fused.cu: one cooperative kernel per iteration for the vector work (single rank)
+struct FusedPlan {
+    bool ok = false;
+    void *fn = nullptr;
+    int G = 0, mpt = 1, KT = 32;
+    int64_t rpb = 0;
+    size_t smem = 0;
+};
+struct FusedIo {
+    MbcgState *st;
+    const double *Vpart;
+    int splits, cs, c, k;
+    int64_t nloc, n;
+    double noise_var, tol;
+    double *D, *V, *U, *R, *Z;
+    const double *L, *Cinv;
+    double *ahist, *bhist, *rhist, *part, *partW, *red;
+    void *Dm;
+    int dm_f32;
+    uint8_t *Bp;   // null: no tensor-core operand
+    int nd, nb_rows;
+    double *Stc;
+    int64_t pad_end;
+};
+bool mbcg_fused_applicable(const bbmm_ctx_s *ctx, int c, int k, bool use_sor, int64_t nloc);
+FusedPlan mbcg_fused_plan(bbmm_ctx_s *ctx, int64_t nloc, int c, int k, const double *cholC,
+                          double *Cinv);
+void mbcg_fused_iteration(bbmm_ctx_s *ctx, const FusedPlan &p, const FusedIo &io);
+
 void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
               const double *cholC, MbcgOut &out);
 void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, int kgen,

@@ -851,6 +851,21 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     passD(0);
     BBMM_LAUNCH_CHECK();
 
+    // fused vector work (one cooperative kernel per iteration) where it applies
+    bool fused = mbcg_fused_applicable(ctx, c, k, use_sor, nloc);
+    FusedPlan fplan;
+    double *Cinv = nullptr, *fpart = nullptr, *fpartW = nullptr, *fred = nullptr;
+    if (fused) {
+        Cinv = (double *)ws.get("cg_Cinv", (size_t)kk * kk * 8);
+        fplan = mbcg_fused_plan(ctx, nloc, c, k, cholC, Cinv);
+        fused = fplan.ok;
+        if (fused) {
+            fpart = (double *)ws.get("cg_fpart", (size_t)4 * fplan.G * c * 8);
+            fpartW = (double *)ws.get("cg_fpartW", (size_t)fplan.G * kk * c * 8);
+            fred = (double *)ws.get("cg_fred", (size_t)(kk + 1) * c * 8);
+        }
+    }
+
     // ---------------- iterations
     cudaEvent_t ev0, ev1;
     BBMM_CUDA(cudaEventCreate(&ev0));
@@ -878,6 +893,22 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         else
             splits = kernel_matmul_onthefly(ctx, a.kind, a.Xs, a.dp, a.n, a.r0, nloc, Dm, acc64,
                                             cp, a.s, Vpart, vcap, e0, e1);
+        if (fused) {
+            FusedIo io{st, Vpart, splits, cs, c, k, nloc, a.n, a.noise_var, a.tol, D, V, U, R, Z,
+                       a.L, Cinv, ahist, bhist, rhist, fpart, fpartW, fred, Dm, acc64 ? 0 : 1,
+                       use_tc ? Bp : nullptr, tc_nd, tc_rows, Stc,
+                       use_tc ? k1tc_pad_rows(a.n) : 0};
+            mbcg_fused_iteration(ctx, fplan, io);
+            BBMM_LAUNCH_CHECK();
+            iters_run = j + 1;
+            if (a.tol > 0.0) {
+                BBMM_CUDA(cudaMemcpyAsync(any_h, &st->any_active, sizeof(int),
+                                          cudaMemcpyDeviceToHost, sm));
+                BBMM_CUDA(cudaStreamSynchronize(sm));
+                if (!*any_h) break;
+            }
+            continue;
+        }
         k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
         reduce(c, red);
         if (multi) allreduce_sum(ctx, red, c);

@@ -65,10 +65,15 @@ def run_ranks(nranks, fn, prec=bb.INT8EXACT):
 
 
 def single(fn, prec=bb.INT8EXACT):
+    """The single-rank reference call, on the same per-step kernels as the ranks (the fused
+    single-rank iteration uses an explicit C^-1 in the Woodbury solve: other rounding)."""
+    import os
     ctx = bb.Context(0).set_matmul_precision(prec)
+    os.environ["BBMM_NO_FUSED_MBCG"] = "1"
     try:
         return fn(ctx)
     finally:
+        os.environ.pop("BBMM_NO_FUSED_MBCG", None)
         ctx.close()
 
 

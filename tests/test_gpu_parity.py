@@ -101,14 +101,15 @@ def test_pivchol_early_stop_at_numerical_rank(ctx, orc):
 
 
 # ------------------------------------------------------------------- mBCG
-# (C2, k = 0) is regime B: unpreconditioned Matern-5/2 ARD, the oracle's
-# relres is far above rounding at p, and the Krylov iterate amplifies per-iteration rounding of D
-# by orders of magnitude.  There the 1e-4 solve bar holds for fp64 search directions (FP64ACC);
-# the tensor-core path (39-bit D) is held to the regime-B stress bar 1e-2.
+# (C2, k = 0) is regime B: unpreconditioned Matern-5/2 ARD, relres
+# 0.02-0.15 at p, and the Krylov iterate amplifies rounding differences by ~1e4 per iteration
+# from iteration 7 on (scripts/diag_fused.py: two fp64 runs that differ only in summation order
+# agree to 1e-16 in alpha_0..alpha_2 and by 1e-3 at alpha_9).  No fixed summation order is
+# "the" answer there, so both precisions are held to the regime-B stress bar 1e-2.
 @pytest.mark.parametrize("name,n,k,prec,bar", [
     ("C0", 256, 5, bb.INT8EXACT, 1e-4), ("C1", 1500, 5, bb.INT8EXACT, 1e-4),
-    ("C4", 3000, 30, bb.INT8EXACT, 1e-4), ("C2", 1200, 0, bb.FP64ACC, 1e-4),
-    ("C2", 1200, 0, bb.INT8EXACT, 1e-2)])
+    ("C4", 3000, 30, bb.INT8EXACT, 1e-4), ("C4", 3000, 30, bb.FP64ACC, 1e-4),
+    ("C2", 1200, 0, bb.FP64ACC, 1e-2), ("C2", 1200, 0, bb.INT8EXACT, 1e-2)])
 def test_mbcg_matches_oracle(ctx, orc, name, n, k, prec, bar):
     cfg = synth.scaled(synth.CONFIGS[name], n)
     pr = synth.make_problem(cfg, seed=1)
@@ -362,3 +363,23 @@ def test_kernel_matmul_tile_edges(ctx, orc, kmode, n):
     err = np.abs(V - ref)
     bound = matmul_bound(orc, pr, D)
     assert np.all(err <= bound), float((err / bound).max())
+
+
+@pytest.mark.parametrize("name,n,kmode", [("C4", 3000, bb.ONTHEFLY), ("C1", 3338, bb.STORED),
+                                          ("C2", 2500, bb.ONTHEFLY), ("C0", 256, bb.ONTHEFLY)])
+def test_fused_iteration_matches_per_step_kernels(ctx, orc, name, n, kmode, monkeypatch):
+    """The single-rank fused mBCG iteration (mbcg_fused.cu, one cooperative kernel) against the
+    per-step kernels (BBMM_NO_FUSED_MBCG=1) and the oracle: same algorithm, other rounding
+    (explicit C^-1 Woodbury, block-ordered sums)."""
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr, g, o = run_both(ctx, orc, cfg, kmode=kmode)
+    monkeypatch.setenv("BBMM_NO_FUSED_MBCG", "1")
+    _, gs, _ = run_both(ctx, orc, cfg, kmode=kmode)
+    monkeypatch.delenv("BBMM_NO_FUSED_MBCG")
+    Uf, Us = g["U"].cpu().numpy(), gs["U"].cpu().numpy()
+    assert colwise_rel(Uf, Us).max() < 1e-5
+    assert abs(g["mll"] - gs["mll"]) <= 1e-7 * abs(gs["mll"])
+    assert np.linalg.norm(g["grad"] - gs["grad"]) <= 1e-5 * np.linalg.norm(gs["grad"])
+    np.testing.assert_allclose(g["stats"]["logdet"], gs["stats"]["logdet"], rtol=1e-8)
+    assert colwise_rel(Uf, o["U"]).max() < 1e-4
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
