@@ -261,15 +261,30 @@ def main():
         tj = json.load(open(tp))
         if tj.get("kernel_path") == path:     # measured for the kernel timed here
             traffic = tj.get("dram_bytes_per_launch")
-    kname = {0: "k1_onthefly (CUDA-core Khat*D)", 1: "k2_stored (Khat*D)",
-             2: "k1tc2_rbf (tcgen05 exact Khat*D)"}[path]
-    roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
-                "peak": peak_exp, "unit": "Gop/s (MUFU ex2/sqrt)", "frac": achieved / peak_exp,
-                "traffic": traffic,
-                "peak_source": f"derived: 16 MUFU ops/clk/SM x 148 SMs x {f_mhz:.0f} MHz "
-                               f"(sm_max_mhz of MEASURED_PEAKS.json, {src})",
-                "kernel_ms": mm_ms,
-                "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
+    kname = {0: "k1_onthefly (CUDA-core Khat*D)", 1: "k2_stored (fp32 K, CUDA-core Khat*D)",
+             2: "k1tc2_rbf (tcgen05 exact Khat*D)",
+             3: "k2tc_stored (int8-slice K on tcgen05, exact Khat*D)"}[path]
+    if path in (1, 3):
+        # stored K: HBM-bound, algorithmic bytes = the stored representation per launch
+        nloc = -(-cfg.n // world)
+        if path == 3:
+            byts = 4.0 * (-(-nloc // 128) * 128) * (-(-cfg.n // 384) * 384)
+        else:
+            byts = 4.0 * nloc * (-(-cfg.n // 4) * 4)
+        gbs = byts / (mm_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": gbs, "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": gbs / pk["hbm_gbs"], "traffic": traffic,
+                    "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({src})",
+                    "kernel_ms": mm_ms,
+                    "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
+    else:
+        roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
+                    "peak": peak_exp, "unit": "Gop/s (MUFU ex2/sqrt)", "frac": achieved / peak_exp,
+                    "traffic": traffic,
+                    "peak_source": f"derived: 16 MUFU ops/clk/SM x 148 SMs x {f_mhz:.0f} MHz "
+                                   f"(sm_max_mhz of MEASURED_PEAKS.json, {src})",
+                    "kernel_ms": mm_ms,
+                    "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
     launches = int(np.sum([s["gpu_launches"] for s in stats]))
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
