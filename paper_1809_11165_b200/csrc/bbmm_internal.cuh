@@ -6,6 +6,7 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -115,6 +116,20 @@ namespace bbmm {
 
 // --------------------------------------------------------------- helpers
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Function attributes (cudaFuncSetAttribute) are per device: a call site runs its setup once
+// per device it launches on (several contexts / devices may share the process).  Racing
+// threads may both run the idempotent setup.
+struct DeviceOnce {
+    std::atomic<uint64_t> mask{0};
+    template <typename F>
+    void operator()(int dev, F &&f) {
+        const uint64_t bit = 1ull << (dev & 63);
+        if (mask.load(std::memory_order_acquire) & bit) return;
+        f();
+        mask.fetch_or(bit, std::memory_order_acq_rel);
+    }
+};
 
 struct RowRange {
     int64_t r0, r1, nb;

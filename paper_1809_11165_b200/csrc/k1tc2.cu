@@ -568,12 +568,11 @@ static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const u
     const int64_t tps = ceil_div(ntiles, sp);
     sp = ceil_div(ntiles, tps);
     BBMM_REQUIRE((size_t)sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k1tc2)");
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    attr(ctx->device, [] {
         BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
-        attr = true;
-    }
+    });
     dim3 grid((unsigned)rb, (unsigned)sp);
     tc2::k1tc2_rbf<C, DA, MODE><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(
         Xa, XB, Bp, S, r0, nloc, tps, ntiles, s, Vpart);

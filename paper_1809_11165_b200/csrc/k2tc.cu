@@ -342,12 +342,11 @@ static int launch(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const d
     using K = Cfg<C>;
     const Plan p = plan(nloc, npad);
     BBMM_REQUIRE((size_t)p.sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k2tc)");
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    attr(ctx->device, [] {
         BBMM_CUDA(cudaFuncSetAttribute(k2tc_stored<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        K::SMEM));
-        attr = true;
-    }
+    });
     k2tc_stored<C><<<p.grid, kThreads, K::SMEM, ctx->stream>>>(Kq, Bp, S, nloc, p.rbs, p.ntiles,
                                                                 p.sp, p.tps, s, Vpart);
     BBMM_LAUNCH_CHECK();

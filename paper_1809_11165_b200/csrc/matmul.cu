@@ -230,12 +230,12 @@ template <int CP, bool ACC64>
 static void launch_k2(bbmm_ctx_s *ctx, dim3 grid, const float *Kst, int64_t n, int64_t nloc,
                       int64_t ldk, const void *Dm, int64_t jchunk, double *Vpart) {
     const size_t smem = (size_t)CP * 128 * (ACC64 ? 8 : 4);
-    static bool attr_set = false;
-    if (!attr_set && smem > 48 * 1024) {
-        BBMM_CUDA(cudaFuncSetAttribute(k2_stored<CP, ACC64>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
+    static DeviceOnce attr;
+    if (smem > 48 * 1024)
+        attr(ctx->device, [&] {
+            BBMM_CUDA(cudaFuncSetAttribute(k2_stored<CP, ACC64>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        });
     k2_stored<CP, ACC64><<<grid, 256, smem, ctx->stream>>>(Kst, n, nloc, ldk, Dm, jchunk, Vpart);
 }
 

@@ -743,13 +743,12 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             const int KT = K <= 256 ? 32 : 16;
             const int64_t rpb = ceil_div(ceil_div(std::max<int64_t>(nloc, 1), ltr_blocks), KT) * KT;
             const size_t smem2 = ((size_t)KT * K + (size_t)KT * c) * 8;
-            static bool attr2 = false;
-            if (!attr2) {
+            static DeviceOnce attr2;
+            attr2(ctx->device, [] {
                 for (auto f : {k_LtR2<1>, k_LtR2<2>, k_LtR2<4>, k_LtR2<8>, k_LtR2<12>, k_LtR2<16>})
                     BBMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    100 * 1024));
-                attr2 = true;
-            }
+            });
             auto f = need <= 1 ? k_LtR2<1> : need <= 2 ? k_LtR2<2> : need <= 4 ? k_LtR2<4>
                    : need <= 8 ? k_LtR2<8> : need <= 12 ? k_LtR2<12> : k_LtR2<16>;
             f<<<ltr_blocks, 256, smem2, sm>>>(Lp, a.n, a.r0, K, Rp, nloc, c, rpb, KT, part_out);
