@@ -50,6 +50,27 @@ def work_per_matmul(cfg):
     return pairs, 2.0 * pairs * c
 
 
+def tensor_frac(cfg, world, mm_ms, pk, detail=False):
+    """Tensor-pipe work of one K1-TC launch: per 128 x 128 tile a 3xTF32
+    distance MMA (K = 3 DA, DA = round8(d + 2)) and 3 int8 MMAs (N = ND round(c + 1), K = 128),
+    as dense-bf16-equivalent flops (tf32 x2, int8 x0.5) over the launch time vs the measured
+    bf16 peak."""
+    c1 = cfg.t + 2
+    da = -(-(cfg.d + 2) // 8) * 8
+    if cfg.kind == synth.RBF:
+        nb = 4 * (-(-c1 // 4) * 4)
+    else:                                           # Matern: five D slices, BLK = round16
+        nb = 5 * (-(-c1 // 16) * 16)
+    rows = -(-(-(-cfg.n // world)) // 128) * 128
+    cols = -(-cfg.n // 128) * 128
+    tf32 = 2.0 * rows * cols * 3 * da
+    i8 = 2.0 * rows * cols * nb * 3
+    eq = 2.0 * tf32 + 0.5 * i8
+    ach = eq / (mm_ms * 1e-3) / 1e12
+    peak = pk.get("bf16_tflops", 1590.0)
+    return (ach / peak, ach, peak) if detail else ach / peak
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -276,6 +297,16 @@ def main():
                     "unit": "GB/s", "frac": gbs / pk["hbm_gbs"], "traffic": traffic,
                     "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({src})",
                     "kernel_ms": mm_ms,
+                    "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
+    elif path == 2 and tensor_frac(cfg, world, mm_ms, pk) > achieved / peak_exp:
+        # K1-TC where the tensor pipe, not the MUFU, binds (large d / many columns: C3)
+        tf, tach, tpk = tensor_frac(cfg, world, mm_ms, pk, detail=True)
+        roofline = {"bound": "tensor", "kernel": kname, "achieved": tach, "peak": tpk,
+                    "unit": "TFLOP/s (dense-bf16 equivalent)", "frac": tf, "traffic": traffic,
+                    "peak_source": "bf16_tflops of MEASURED_PEAKS.json; tf32 work counted x2 and "
+                                   "int8 work x0.5 (nominal B200 dense rates 1.1 / 2.25 / 4.5 "
+                                   "PFLOP/s, B200_PROFILING.md)",
+                    "mufu_frac": achieved / peak_exp, "kernel_ms": mm_ms,
                     "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
     else:
         roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
