@@ -155,3 +155,44 @@ def test_mbcg_partitioned_rows(orc):
     assert colwise_rel(U, one["U"].cpu().numpy()).max() < 1e-6
     np.testing.assert_allclose(parts[0]["alpha"][:5], one["alpha"][:5], rtol=1e-9)
     np.testing.assert_array_equal(parts[0]["alpha"], parts[1]["alpha"])
+
+
+@pytest.mark.parametrize("name,n,kmode", [("C4", 3000, bb.ONTHEFLY), ("C1", 2000, bb.STORED)])
+def test_predict_partitioned_matches_single_rank(orc, name, n, kmode):
+    """Row f1 on the partitioned path: every rank returns the same mean / variance for all test
+    points, equal to the single-rank call."""
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=5)
+    Xs = dev(synth.test_points(cfg, 20, seed=9))
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        m, v = bb.predict(ctx, X, y, Xs, h, cfg.k, max_iter=cfg.p, kmode=kmode)
+        return m.cpu().numpy(), v.cpu().numpy()
+
+    parts = run_ranks(2, call)
+    ms, vs = single(call)
+    for m, v in parts:
+        np.testing.assert_array_equal(m, parts[0][0])
+        np.testing.assert_array_equal(v, parts[0][1])
+    s = np.exp(pr.log_s)
+    assert np.abs(parts[0][0] - ms).max() <= 1e-6 * max(np.abs(ms).max(), 1e-3)
+    assert np.abs(parts[0][1] - vs).max() <= 1e-6 * s
+
+
+def test_train_adam_partitioned_matches_single_rank(orc):
+    """Row f2 on the partitioned path: identical trained theta on every rank, equal to the
+    single-rank trainer up to reduction order."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 2000)
+    pr = synth.make_problem(cfg, seed=6)
+    X, y, h0 = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        h1, tr = bb.train_adam(ctx, X, y, h0, cfg.t, cfg.k, cfg.p, steps=3, seed=3)
+        return np.concatenate([np.atleast_1d(h1.log_ls), [h1.log_s, h1.log_noise]]), tr
+
+    parts = run_ranks(2, call)
+    th1, tr1 = single(call)
+    np.testing.assert_array_equal(parts[0][0], parts[1][0])
+    np.testing.assert_allclose(parts[0][0], th1, rtol=0, atol=1e-8)
+    np.testing.assert_allclose(parts[0][1][:, 0], tr1[:, 0], rtol=1e-8)

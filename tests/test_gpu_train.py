@@ -32,12 +32,15 @@ def dev(a, dtype=torch.float32):
     return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
 
 
-@pytest.mark.parametrize("name,n,steps", [("C0", 256, 5), ("C4", 3000, 4), ("C2", 1200, 3)])
-def test_train_matches_oracle(ctx, orc, name, n, steps):
+@pytest.mark.parametrize("name,n,steps,kmode", [("C0", 256, 5, bb.ONTHEFLY), ("C4", 3000, 4, bb.ONTHEFLY),
+                                                ("C2", 1200, 3, bb.ONTHEFLY),
+                                                ("C1", 2000, 3, bb.STORED)])
+def test_train_matches_oracle(ctx, orc, name, n, steps, kmode):
     cfg = synth.scaled(synth.CONFIGS[name], n)
     pr = synth.make_problem(cfg, seed=6)
     h0 = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
-    h1, tr = bb.train_adam(ctx, dev(pr.X), dev(pr.y), h0, cfg.t, cfg.k, cfg.p, steps=steps, seed=3)
+    h1, tr = bb.train_adam(ctx, dev(pr.X), dev(pr.y), h0, cfg.t, cfg.k, cfg.p, steps=steps, seed=3,
+                           kmode=kmode)
     tho, tro = orc.train_adam(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, cfg.t, cfg.k,
                               cfg.p, steps, seed=3)
     th = np.concatenate([np.atleast_1d(h1.log_ls), [h1.log_s, h1.log_noise]])
