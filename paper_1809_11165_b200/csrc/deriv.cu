@@ -76,17 +76,20 @@ k7_deriv(const float *__restrict__ Xs, const float *__restrict__ A32,
             for (int q = 0; q <= D; q++) s32[q] = 0.0f;
 #pragma unroll 2
             for (int jj = jf; jj < jf + FOLD; jj++) {
+                // four independent partial sums each for r^2 and W (instruction-level
+                // parallelism: the single chains were latency-bound at low occupancy)
                 float dq[D];
-                float rs2 = 0.0f;
+                float r4[4] = {0.0f, 0.0f, 0.0f, 0.0f}, w4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
                 for (int q = 0; q < D; q++) {
                     float df = xi[q] - xs[jj][q];
                     dq[q] = df * df;
-                    rs2 += dq[q];
+                    r4[q & 3] += dq[q];
                 }
-                float w = 0.0f;
+                const float rs2 = (r4[0] + r4[1]) + (r4[2] + r4[3]);
 #pragma unroll
-                for (int c = 0; c < CP; c++) w = fmaf(ai[c], bs[jj][c], w);
+                for (int c = 0; c < CP; c++) w4[c & 3] = fmaf(ai[c], bs[jj][c], w4[c & 3]);
+                const float w = (w4[0] + w4[1]) + (w4[2] + w4[3]);
                 float kv, g;
                 kval_and_dfac<KIND>(rs2, kv, g);
                 float gw = g * w;
@@ -98,9 +101,10 @@ k7_deriv(const float *__restrict__ Xs, const float *__restrict__ A32,
             for (int q = 0; q <= D; q++) s64[q] += (double)s32[q];
         }
     }
-    // block reduction of the D+1 accumulators (fixed order)
+    // block reduction of the D+1 accumulators (fixed order); fully unrolled so that s64
+    // stays in registers (a runtime index would move it to local memory)
     const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-#pragma unroll 1
+#pragma unroll
     for (int q = 0; q <= D; q++) {
         __syncthreads();
         red[tid] = s64[q];
