@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 namespace bbmm {
 namespace fz {
 
-constexpr int kT = 256;          // threads per block
+constexpr int kT = 512;          // threads per block (16 warps: enough loads in flight for HBM)
 constexpr int kCW = 32;          // column lanes of the element-wise passes (c <= 20)
 constexpr int kRB = kT / kCW;    // rows per sweep
 constexpr int kCM = 20;          // max columns of the fused path
@@ -425,7 +425,9 @@ void *fused_fn() { return (void *)fz::k_mbcg_fused<MPT>; }
 // kernels; C2, n = 45 730: even; C1: 2.06 vs 2.9 ms).
 constexpr int64_t kFusedMaxRows = 65536;
 bool mbcg_fused_applicable(const bbmm_ctx_s *ctx, int c, int k, bool use_sor, int64_t nloc) {
-    if (ctx->nranks != 1 || use_sor || c > fz::kCM || k > kMaxRank || nloc > kFusedMaxRows)
+    const char *mx = getenv("BBMM_FUSED_MAX_ROWS");      // experiment override
+    const int64_t max_rows = mx ? atoll(mx) : kFusedMaxRows;
+    if (ctx->nranks != 1 || use_sor || c > fz::kCM || k > kMaxRank || nloc > max_rows)
         return false;
     const char *env = getenv("BBMM_NO_FUSED_MBCG");
     return !(env && env[0] == '1');
