@@ -75,16 +75,24 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  * FP32ACC: D rounded to fp32, products summed in fp32 over 16 terms then
  *   folded into fp64.  Faster; parity holds only where mBCG has converged
  *   (SURVEY.md §8c "regime A"). */
-/* INT8EXACT (default): tcgen05 tensor cores; kernel values as 22-bit fixed
- *   point, D as 31-bit fixed point (per-column scale), products and sums EXACT
- *   in int32 (drained to fp64); the exponent comes from a 3xTF32 tensor-core
- *   distance.  Used for on-the-fly RBF when the shape is supported (d <= 22,
- *   t + 1 in {1,2,4,8,11}; d <= 6 for t + 1 = 17) and
- *   max |x_scaled|^2 <= 16 (precision guard); otherwise FP64ACC is used. */
+/* INT8EXACT (default): tcgen05 tensor cores, products and sums EXACT in
+ *   int32 (drained to fp64).  On the fly (RBF, isotropic or ARD): kernel values
+ *   as 22-bit fixed point, D as 31-bit fixed point (per-column scale), the
+ *   exponent from a 3xTF32 tensor-core distance; shapes t + 1 in {1,2,4,8} with
+ *   d <= 22 and t + 1 in {11,17,33} with d <= 30, and max |x_scaled|^2 <= 16
+ *   (precision guard).  Stored K (BBMM_STORED, t + 1 in {1,2,4,8,11,16,17,32,33}):
+ *   K as 30-bit and D as 39-bit fixed point.  Everything else (Matern on the
+ *   fly included) uses FP64ACC.
+ * INT8FAST: INT8EXACT plus Matern-5/2 on the fly on the tensor cores (22-bit
+ *   kernel values, 39-bit D, t + 1 in {11,17}, d <= 14): 3.8x faster than
+ *   FP64ACC at the C2 shape, but the 22-bit kernel values move the gradient of
+ *   mildly unconverged Matern problems past the 1e-3 parity bar (C2 shape,
+ *   n = 3000: 1.1e-3), hence opt-in. */
 typedef enum {
     BBMM_MATMUL_FP64ACC = 0,
     BBMM_MATMUL_FP32ACC = 1,
-    BBMM_MATMUL_INT8EXACT = 2
+    BBMM_MATMUL_INT8EXACT = 2,
+    BBMM_MATMUL_INT8FAST = 3
 } bbmm_matmul_precision_t;
 
 typedef struct {

@@ -362,10 +362,11 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
 
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p) {
     if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC &&
-                 p != BBMM_MATMUL_INT8EXACT))
+                 p != BBMM_MATMUL_INT8EXACT && p != BBMM_MATMUL_INT8FAST))
         return BBMM_ERR_ARG;
     ctx->matmul_acc64 = (p != BBMM_MATMUL_FP32ACC);
-    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT);
+    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT || p == BBMM_MATMUL_INT8FAST);
+    ctx->matmul_fast = (p == BBMM_MATMUL_INT8FAST);
     return BBMM_OK;
 }
 
@@ -631,12 +632,18 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                 ctx->launches++;
             }
             allgather_rows(ctx, B32, (size_t)rr.nb * cs * 4);
+            const bool dtc = ctx->matmul_tc && deriv_tc_supported(h.kind, dp, cp, n);
             double *dpart = (double *)ws.get(
-                "d_part", derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp) * 8);
+                "d_part", std::max(derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp),
+                                   deriv_tc_part_elems(n, std::max<int64_t>(nloc, 1), dp)) * 8);
             if (nloc > 0) {
                 int nblk = 0;
-                derivative_pass(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, nq, h.n_ls > 1,
-                                d, dpart, &nblk);
+                if (dtc)   // W tiles on the tensor cores (deriv_tc.cu)
+                    nblk = derivative_pass_tc(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, c,
+                                              dpart);
+                else
+                    derivative_pass(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, nq,
+                                    h.n_ls > 1, d, dpart, &nblk);
                 reduce_blocks(ctx, dpart, nblk, nq, dred);
                 k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
                 ctx->launches++;

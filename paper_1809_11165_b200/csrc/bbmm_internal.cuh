@@ -108,6 +108,7 @@ struct bbmm_ctx_s {
     int launches = 0;   // library kernel launches since last reset
     bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
+    bool matmul_fast = false;   // BBMM_MATMUL_INT8FAST: also Matern on the fly (22-bit k)
     int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
     bbmm::LocalGroup *local = nullptr;   // in-process rank group (comm_local.cu) instead of NCCL
 };
@@ -304,6 +305,12 @@ void derivative_pass(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t
                      int64_t r0, int64_t nloc, const float *A32, const float *B32, int cp,
                      int nq_out, bool ard, int d, double *part, int *nblocks_out);
 size_t derivative_part_elems(int64_t n, int64_t nloc, int dp);
+// deriv_tc.cu: the same pass with the bilinear weights W = A B^T on the tensor cores
+bool deriv_tc_supported(int kind, int dp, int cp, int64_t n);
+size_t deriv_tc_part_elems(int64_t n, int64_t nloc, int dp);
+int derivative_pass_tc(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+                       int64_t nloc, const float *A32, const float *B32, int cp, int c,
+                       double *part);
 void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red);
 
 // ------------------------------------------------------------- comm

@@ -645,7 +645,9 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
     if (!ctx->matmul_tc) return op;
     const int64_t npad = k1tc_pad_rows(npad_rows);
     op.d = d;
-    if (k1tc2_supported(h.kind, d, c)) {
+    // Matern on the fly (22-bit kernel values) only under INT8FAST (include/bbmm.h)
+    const bool allowed = h.kind == BBMM_RBF || ctx->matmul_fast;
+    if (allowed && k1tc2_supported(h.kind, d, c)) {
         float *xa = (float *)ctx->ws.get("tc2_Xa", (size_t)k1tc2_xa_floats(npad, d) * 4);
         float *xb = (float *)ctx->ws.get("tc2_XB", (size_t)k1tc2_xb_floats(npad, d) * 4);
         const float max_sq = k1tc2_prep_inputs(ctx, X, n, d, h, xa, xb, npad);

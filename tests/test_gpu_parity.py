@@ -214,9 +214,11 @@ def test_tensor_core_path_is_selected(ctx, orc):
     pr, g, o = run_both(ctx, orc, cfg3)
     assert g["stats"]["matmul_path"] == 2
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
-    cfg2 = synth.scaled(synth.CONFIGS["C2"], 2500)      # Matern-5/2 ARD on the fly (MODE 2)
+    cfg2 = synth.scaled(synth.CONFIGS["C2"], 2500)      # Matern-5/2 ARD on the fly
     pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
-    assert g["stats"]["matmul_path"] == 2
+    assert g["stats"]["matmul_path"] == 0               # INT8EXACT: FP64ACC for Matern
+    pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY, prec=bb.INT8FAST)
+    assert g["stats"]["matmul_path"] == 2               # INT8FAST: K1-TC MODE 2
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
     assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
     assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
@@ -383,3 +385,56 @@ def test_fused_iteration_matches_per_step_kernels(ctx, orc, name, n, kmode, monk
     np.testing.assert_allclose(g["stats"]["logdet"], gs["stats"]["logdet"], rtol=1e-8)
     assert colwise_rel(Uf, o["U"]).max() < 1e-4
     assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+
+
+@pytest.mark.parametrize("name,n", [("C3", 2500), ("C2", 3000), ("C2", 1001)])
+def test_tensor_core_derivative_pass_matches_oracle(ctx, orc, name, n, monkeypatch):
+    """ARD / Matern derivative pass with W = A B^T on the tensor cores (deriv_tc.cu), forced at
+    oracle-friendly n (config's default operator): gradient vs the oracle at the bar, with the
+    CUDA-core pass's error printed beside it."""
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    monkeypatch.setenv("BBMM_DERIV_TC_MIN_N", "0")
+    pr, g, o = run_both(ctx, orc, cfg)
+    monkeypatch.setenv("BBMM_NO_DERIV_TC", "1")
+    _, gc, _ = run_both(ctx, orc, cfg)
+    e_tc = np.linalg.norm(g["grad"] - o["grad"]) / np.linalg.norm(o["grad"])
+    e_cc = np.linalg.norm(gc["grad"] - o["grad"]) / np.linalg.norm(o["grad"])
+    print(f"{name} n={n}: gradient error vs oracle: tensor-core pass {e_tc:.2e}, CUDA-core {e_cc:.2e}")
+    assert e_tc <= 1e-3
+    assert g["mll"] == gc["mll"]          # only the derivative pass differs
+
+
+def test_tensor_core_derivative_pass_at_c3_size_sample(ctx, orc):
+    """C3 shape at n = 20 000 (the default threshold path, several tiles per CTA): the
+    tensor-core pass against the CUDA-core pass on the same solves."""
+    import os
+    cfg = synth.scaled(synth.CONFIGS["C3"], 20000)
+    pr = synth.make_problem(cfg, seed=0)
+    args = (ctx, dev(pr.X), dev(pr.y), hyper_of(pr), cfg.t, cfg.k, cfg.p)
+    g = bb.mll_and_grad(*args, seed=7)
+    os.environ["BBMM_NO_DERIV_TC"] = "1"
+    try:
+        gc = bb.mll_and_grad(*args, seed=7)
+    finally:
+        os.environ.pop("BBMM_NO_DERIV_TC", None)
+    assert g["mll"] == gc["mll"]
+    # both passes sum fp32 pair terms (16-pair chunks) whose cancellation within each S_q
+    # amplifies rounding: measured 3e-5 relative between them, 1e-3 is the gradient bar
+    assert np.linalg.norm(g["grad"] - gc["grad"]) <= 1e-4 * np.linalg.norm(gc["grad"])
+
+
+@pytest.mark.parametrize("n,c", [(2777, 17), (1500, 11), (700, 17)])
+def test_matern_fast_matmul_matches_oracle(ctx, orc, n, c):
+    """INT8FAST Matern-5/2 kernel-matmul on the tensor cores (K1-TC MODE 2) vs the oracle,
+    held to the matmul bound (fp32 kernel values + 22-bit fixed point)."""
+    pr = synth.make_problem(synth.scaled(synth.CONFIGS["C2"], n), seed=3)
+    D = synth.random_block(n, c, seed=4).astype(np.float64)
+    ctx.set_matmul_precision(bb.INT8FAST)
+    try:
+        V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr)).cpu().numpy()
+    finally:
+        ctx.set_matmul_precision(bb.INT8EXACT)
+    ref = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
+    err = np.abs(V - ref)
+    bound = matmul_bound(orc, pr, D)
+    assert np.all(err <= bound), float((err / bound).max())
