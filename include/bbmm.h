@@ -84,10 +84,10 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   K as 30-bit and D as 39-bit fixed point.  Everything else (Matern on the
  *   fly included) uses FP64ACC.
  * INT8FAST: INT8EXACT plus Matern-5/2 on the fly on the tensor cores (22-bit
- *   kernel values, 39-bit D, t + 1 in {11,17}, d <= 14): 3.8x faster than
- *   FP64ACC at the C2 shape, but the 22-bit kernel values move the gradient of
- *   mildly unconverged Matern problems past the 1e-3 parity bar (C2 shape,
- *   n = 3000: 1.1e-3), hence opt-in. */
+ *   kernel values from the 3xTF32 distance, 39-bit D, t + 1 in {11,17}, d <= 14):
+ *   3.8x faster than FP64ACC at the C2 shape, but its ~1e-7 kernel-value error
+ *   moves mildly unconverged Matern problems past the parity bars (C2 shape,
+ *   n = 3000: solve 1.4e-4, gradient 1.2e-3), hence opt-in. */
 typedef enum {
     BBMM_MATMUL_FP64ACC = 0,
     BBMM_MATMUL_FP32ACC = 1,
