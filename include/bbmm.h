@@ -76,23 +76,19 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   folded into fp64.  Faster; parity holds only where mBCG has converged
  *   (SURVEY.md §8c "regime A"). */
 /* INT8EXACT (default): tcgen05 tensor cores, products and sums EXACT in
- *   int32 (drained to fp64).  On the fly (RBF, isotropic or ARD): kernel values
+ *   int32 (drained to fp64).  On the fly, RBF (isotropic or ARD): kernel values
  *   as 22-bit fixed point, D as 31-bit fixed point (per-column scale), the
  *   exponent from a 3xTF32 tensor-core distance; shapes t + 1 in {1,2,4,8} with
  *   d <= 22 and t + 1 in {11,17,33} with d <= 30, and max |x_scaled|^2 <= 16
- *   (precision guard).  Stored K (BBMM_STORED, t + 1 in {1,2,4,8,11,16,17,32,33}):
- *   K as 30-bit and D as 39-bit fixed point.  Everything else (Matern on the
- *   fly included) uses FP64ACC.
- * INT8FAST: INT8EXACT plus Matern-5/2 on the fly on the tensor cores (22-bit
- *   kernel values from the 3xTF32 distance, 39-bit D, t + 1 in {11,17}, d <= 14):
- *   3.8x faster than FP64ACC at the C2 shape, but its ~1e-7 kernel-value error
- *   moves mildly unconverged Matern problems past the parity bars (C2 shape,
- *   n = 3000: solve 1.4e-4, gradient 1.2e-3), hence opt-in. */
+ *   (precision guard).  On the fly, Matern-5/2: distances from direct fp32
+ *   differences (the expanded form's ~1e-7 error breaks the parity bars there,
+ *   DESIGN.md §6), 22-bit kernel values, 39-bit D; t + 1 in {11,17}, d <= 14.
+ *   Stored K (BBMM_STORED, t + 1 in {1,2,4,8,11,16,17,32,33}): K as 30-bit and D
+ *   as 39-bit fixed point.  Everything else uses FP64ACC. */
 typedef enum {
     BBMM_MATMUL_FP64ACC = 0,
     BBMM_MATMUL_FP32ACC = 1,
-    BBMM_MATMUL_INT8EXACT = 2,
-    BBMM_MATMUL_INT8FAST = 3
+    BBMM_MATMUL_INT8EXACT = 2
 } bbmm_matmul_precision_t;
 
 typedef struct {

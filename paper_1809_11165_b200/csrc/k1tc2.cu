@@ -170,7 +170,11 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[B
 // (= (dK/dlog l)/s for the isotropic RBF, used by the derivative pass);
 // MODE 2: Matern-5/2 k~ = (1 + rh + rh^2/3) e^{-rh}, rh = sqrt(-S) (inputs
 // scaled by sqrt5/l; two MUFU ops per pair: sqrt, ex2), 39-bit D (ND = 5).
-template <int C, int DA, int MODE>
+// MODE 2 computes the distances directly on the FP32 pipes from plain x tiles
+// ([BK][DA] fp32 in the XB ring, zero-padded past d) -- the 3xTF32 expanded form's
+// ~1e-7 absolute error in r^2 is too large for Matern; DM = the
+// dimensions those loops run over (a compile-time bound, zero padding past d).
+template <int C, int DA, int MODE, int DM = DA>
 __global__ void __launch_bounds__(kThreads, 1)
 k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
           const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
@@ -196,7 +200,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     if (tid == 0) {
         for (int q = 0; q < K::XS; q++) {
             ptx::mbar_init(&full_x[q], 1);
-            ptx::mbar_init(&free_x[q], 1);
+            // MODE 2 reads the x tile on the compute warps (direct distances), not in an MMA
+            ptx::mbar_init(&free_x[q], MODE == 2 ? NCW : 1);
         }
         for (int q = 0; q < K::QS; q++) {
             ptx::mbar_init(&full_q[q], 1);
@@ -264,6 +269,13 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             const int xi = t % K::XS;
             const int b = t % K::NBUF;
             ptx::tc_fence_after();
+            if (MODE == 2) {
+                // no distance MMA: only signal that buffer b is free again once the int8
+                // MMAs issued so far (the last readers of b) have completed
+                if (leader) ptx::mma_commit(&s_full[b]);
+                __syncwarp();
+                return;
+            }
             if (leader) {
                 const uint32_t xb = ptx::smem_u32(smem + xi * K::XB_BYTES);
                 const uint32_t ap = ptx::smem_u32(smem + K::AP_OFF);
@@ -281,7 +293,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             __syncwarp();
         };
         for (int t = 0; t < K::NBUF && t < ntl; t++) {
-            wait_x(t);
+            if (MODE != 2) wait_x(t);
             issue_dist(t);
         }
         for (int t = 0; t < ntl; t++) {
@@ -291,7 +303,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             const bool first = (t % TPW) == 0;
             // operands of the next distance MMA: normally resident long ago, so
             // this check overlaps the wait for the compute warps below
-            if (t + K::NBUF < ntl) wait_x(t + K::NBUF);
+            if (MODE != 2 && t + K::NBUF < ntl) wait_x(t + K::NBUF);
             if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
             ptx::mbar_wait(&a_full[b], (uint32_t)((t / K::NBUF) & 1));
             ptx::mbar_wait(&full_q[qi], (uint32_t)((t / K::QS) & 1));
@@ -317,6 +329,14 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const int sub = warp & 3, h = warp >> 2;
         const int64_t row = (int64_t)blockIdx.x * BM + sub * 32 + lane;
         const bool valid = row < nloc;
+        // MODE 2: this row's scaled inputs (plain layout of its XB tile)
+        float xrow[MODE == 2 ? DM : 1];
+        if constexpr (MODE == 2) {
+            const int64_t rg = r0 + row;
+            const float *src = XB + (rg / BK) * (int64_t)(2 * DA * BK) + (rg % BK) * DA;
+#pragma unroll
+            for (int q = 0; q < DM; q++) xrow[q] = valid ? src[q] : 0.0f;
+        }
         const uint32_t lane_base = tmem + ((uint32_t)(sub * 32) << 16);
         if (h == 0) {
             // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32), written to
@@ -416,13 +436,41 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::tc_fence_after();
             uint32_t sv[JW];
             const uint32_t col = my_col + b * BK;
-            if constexpr (JW == 32) {
+            if constexpr (MODE == 2) {
+                // S = -r^2 from direct differences with the tile's x_j (broadcast loads)
+                const int xs = t % K::XS;
+                ptx::mbar_wait(&full_x[xs], (uint32_t)((t / K::XS) & 1));
+                // shared-space 128-bit loads (the aligned smem pointer is generic to the compiler)
+                const uint32_t xt = ptx::smem_u32(smem + xs * K::XB_BYTES) + (JW * h) * DA * 4;
+#pragma unroll
+                for (int jj = 0; jj < JW; jj++) {
+                    float r4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                    for (int q4 = 0; q4 < (DM + 3) / 4; q4++) {
+                        float x[4];
+                        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                                     : "r"(xt + (jj * DA + 4 * q4) * 4));
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int q = 4 * q4 + u;
+                            if (q < DM) {
+                                const float df = xrow[q] - x[u];
+                                r4[u] = fmaf(df, df, r4[u]);
+                            }
+                        }
+                    }
+                    sv[jj] = __float_as_uint(-((r4[0] + r4[1]) + (r4[2] + r4[3])));
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&free_x[xs]);
+            } else if constexpr (JW == 32) {
                 ptx::tmem_ld32(col, *reinterpret_cast<uint32_t(*)[32]>(sv));
             } else {
 #pragma unroll
                 for (int u = 0; u < 4; u++) ptx::tmem_ld4(col + 8 * u, sv + 4 * u);
             }
-            ptx::tmem_ld_wait();
+            if constexpr (MODE != 2) ptx::tmem_ld_wait();
             uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];
 #pragma unroll
             for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
@@ -477,7 +525,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad, int d, int DA,
                            const float *__restrict__ scale, const double *__restrict__ mean,
                            float *__restrict__ Xa, float *__restrict__ XB,
-                           unsigned int *__restrict__ max_sq_bits) {
+                           unsigned int *__restrict__ max_sq_bits, int plain) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npad;
          j += (int64_t)gridDim.x * blockDim.x) {
         float xs[kMaxDim];
@@ -497,6 +545,11 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
                 else if (q == d + 1) { a = 1.0f; b = e; }
             }
             Xa[j * DA + q] = a;
+            if (plain) {   // MODE 2: x_j as fp32 rows [BK][DA] of its tile, zero past d
+                XB[(j / BK) * (int64_t)(2 * DA * BK) + (j % BK) * DA + q] =
+                    (ok && q < d) ? xs[q] : 0.0f;
+                continue;
+            }
             const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
             const float bl = b - bh;
             const int64_t tt = j / BK;
@@ -546,7 +599,7 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
     BBMM_CUDA(cudaMemsetAsync(mx, 0, 4, ctx->stream));
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(npad, 256), 4 * kNumSMs));
     tc2::k_prep_tc2<<<grid, 256, 0, ctx->stream>>>(X, n, npad, d, tc2_da(d), sc_d, mean, Xa, XB,
-                                                   mx);
+                                                   mx, h.kind == BBMM_MATERN52 ? 1 : 0);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
     unsigned int mh = 0;
@@ -557,7 +610,7 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
     return mf;
 }
 
-template <int C, int DA, int MODE>
+template <int C, int DA, int MODE, int DM = DA>
 static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                       const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
                       double *Vpart, size_t cap) {
@@ -570,11 +623,11 @@ static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const u
     BBMM_REQUIRE((size_t)sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k1tc2)");
     static DeviceOnce attr;
     attr(ctx->device, [] {
-        BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA, MODE>,
+        BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA, MODE, DM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
     });
     dim3 grid((unsigned)rb, (unsigned)sp);
-    tc2::k1tc2_rbf<C, DA, MODE><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(
+    tc2::k1tc2_rbf<C, DA, MODE, DM><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(
         Xa, XB, Bp, S, r0, nloc, tps, ntiles, s, Vpart);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
@@ -614,7 +667,8 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
     }
     if (mode == 2) {   // Matern-5/2
         if (nloc > 0) {
-            if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            if (c == 17 && d == 9) sp = launch_tc2<17, 16, 2, 9>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            else if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
             else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
             else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
             else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
@@ -645,9 +699,7 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
     if (!ctx->matmul_tc) return op;
     const int64_t npad = k1tc_pad_rows(npad_rows);
     op.d = d;
-    // Matern on the fly (22-bit kernel values) only under INT8FAST (include/bbmm.h)
-    const bool allowed = h.kind == BBMM_RBF || ctx->matmul_fast;
-    if (allowed && k1tc2_supported(h.kind, d, c)) {
+    if (k1tc2_supported(h.kind, d, c)) {
         float *xa = (float *)ctx->ws.get("tc2_Xa", (size_t)k1tc2_xa_floats(npad, d) * 4);
         float *xb = (float *)ctx->ws.get("tc2_XB", (size_t)k1tc2_xb_floats(npad, d) * 4);
         const float max_sq = k1tc2_prep_inputs(ctx, X, n, d, h, xa, xb, npad);

@@ -5,8 +5,8 @@ SLQ, derivative pass) is run after a warm-up call; the library's own CUDA events
 time per launch (ms_matmul / matmul_launches).  Operators:
   stored_int8  -- BBMM_STORED, INT8EXACT: K as four u8 slices (30-bit fixed point), tcgen05 (k2tc)
   stored_fp32  -- BBMM_STORED, FP64ACC:   K as fp32 (4 B per entry), CUDA-core DFMA (k2_stored)
-  onthefly     -- BBMM_ONTHEFLY, default precision (tcgen05 for RBF; FP64ACC for Matern)
-  onthefly_int8fast -- BBMM_ONTHEFLY, INT8FAST (Matern on tcgen05, 22-bit kernel values)
+  onthefly     -- BBMM_ONTHEFLY, default precision (tcgen05 where the kernel supports the shape)
+  onthefly_fp64acc -- BBMM_ONTHEFLY, FP64ACC (CUDA-core DFMA)
 Roofline of the stored variants: HBM, algorithmic bytes per launch = bytes of the stored
 representation (4 x n_loc_pad x n_pad for the int8 slices, 4 x n_loc x n for fp32) / per-launch time vs MEASURED_PEAKS.json hbm_gbs.
 One JSON line per (config, operator).  usage: python scripts/bench_stored.py [C2|C1 ...]"""
@@ -40,7 +40,7 @@ def main(names):
         for label, kmode, prec in [("stored_int8", bb.STORED, bb.INT8EXACT),
                                    ("stored_fp32", bb.STORED, bb.FP64ACC),
                                    ("onthefly", bb.ONTHEFLY, bb.INT8EXACT),
-                                   ("onthefly_int8fast", bb.ONTHEFLY, bb.INT8FAST)]:
+                                   ("onthefly_fp64acc", bb.ONTHEFLY, bb.FP64ACC)]:
             ctx.set_matmul_precision(prec)
             try:
                 runs = []

@@ -1,4 +1,4 @@
-"""Gradient / solve error vs the oracle of the on-the-fly Matern tensor-core path (INT8FAST)
+"""Gradient / solve error vs the oracle of the on-the-fly Matern tensor-core path (K1-TC MODE 2)
 against FP64ACC and the stored path at the C2 shape (small n).  python scripts/diag_matern_fast.py"""
 import os, sys
 import numpy as np, torch
@@ -13,7 +13,7 @@ for n in (2048, 2500, 3000):
     X = torch.from_numpy(pr.X).cuda(); y = torch.from_numpy(pr.y).cuda()
     h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
     o = oracle.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, cfg.t, cfg.k, cfg.p, seed=7)
-    for lab, km, pc in [("fast_otf", bb.ONTHEFLY, bb.INT8FAST), ("fp64acc_otf", bb.ONTHEFLY, bb.FP64ACC),
+    for lab, km, pc in [("tc_otf", bb.ONTHEFLY, bb.INT8EXACT), ("fp64acc_otf", bb.ONTHEFLY, bb.FP64ACC),
                         ("int8_stored", bb.STORED, bb.INT8EXACT)]:
         ctx.set_matmul_precision(pc)
         g = bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=7, kmode=km, return_solves=True)

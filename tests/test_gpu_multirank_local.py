@@ -81,8 +81,8 @@ CASES = [  # name, n, kmode, prec, nranks, expected matmul path
     ("C4", 3000, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
     ("C4", 3000, bb.ONTHEFLY, bb.INT8EXACT, 3, 2),
     ("C1", 3338, bb.STORED, bb.INT8EXACT, 2, 3),
-    ("C2", 2500, bb.ONTHEFLY, bb.INT8FAST, 2, 2),     # Matern on the fly on tcgen05 (opt-in)
-    ("C2", 2500, bb.ONTHEFLY, bb.INT8EXACT, 2, 0),    # default: FP64ACC for Matern
+    ("C2", 2500, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),    # Matern on the fly on tcgen05 (MODE 2)
+    ("C2", 2500, bb.ONTHEFLY, bb.FP64ACC, 2, 0),
     ("C3", 2000, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
     ("C4", 3000, bb.ONTHEFLY, bb.FP64ACC, 2, 0),
     ("C4", 300, bb.ONTHEFLY, bb.INT8EXACT, 4, 2),     # n = 300, nb = 128: rank 3 owns no rows

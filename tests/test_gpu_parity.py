@@ -214,11 +214,10 @@ def test_tensor_core_path_is_selected(ctx, orc):
     pr, g, o = run_both(ctx, orc, cfg3)
     assert g["stats"]["matmul_path"] == 2
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
-    cfg2 = synth.scaled(synth.CONFIGS["C2"], 2500)      # Matern-5/2 ARD on the fly
-    pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
-    assert g["stats"]["matmul_path"] == 0               # INT8EXACT: FP64ACC for Matern
-    pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY, prec=bb.INT8FAST)
-    assert g["stats"]["matmul_path"] == 2               # INT8FAST: K1-TC MODE 2
+    for n2 in (2500, 3000):                             # Matern-5/2 ARD on the fly (MODE 2)
+        cfg2 = synth.scaled(synth.CONFIGS["C2"], n2)
+        pr, g, o = run_both(ctx, orc, cfg2, kmode=bb.ONTHEFLY)
+        assert g["stats"]["matmul_path"] == 2
     assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
     assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
     assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
@@ -424,16 +423,12 @@ def test_tensor_core_derivative_pass_at_c3_size_sample(ctx, orc):
 
 
 @pytest.mark.parametrize("n,c", [(2777, 17), (1500, 11), (700, 17)])
-def test_matern_fast_matmul_matches_oracle(ctx, orc, n, c):
-    """INT8FAST Matern-5/2 kernel-matmul on the tensor cores (K1-TC MODE 2) vs the oracle,
-    held to the matmul bound (fp32 kernel values + 22-bit fixed point)."""
+def test_matern_tc_matmul_matches_oracle(ctx, orc, n, c):
+    """Matern-5/2 kernel-matmul on the tensor cores (K1-TC MODE 2, direct distances) vs the
+    oracle, held to the matmul bound (fp32 kernel values + 22-bit fixed point)."""
     pr = synth.make_problem(synth.scaled(synth.CONFIGS["C2"], n), seed=3)
     D = synth.random_block(n, c, seed=4).astype(np.float64)
-    ctx.set_matmul_precision(bb.INT8FAST)
-    try:
-        V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr)).cpu().numpy()
-    finally:
-        ctx.set_matmul_precision(bb.INT8EXACT)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr)).cpu().numpy()
     ref = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
     err = np.abs(V - ref)
     bound = matmul_bound(orc, pr, D)
