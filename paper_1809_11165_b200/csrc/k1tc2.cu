@@ -333,9 +333,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         float xrow[MODE == 2 ? DM : 1];
         if constexpr (MODE == 2) {
             const int64_t rg = r0 + row;
-            const float *src = XB + (rg / BK) * (int64_t)(2 * DA * BK) + (rg % BK) * DA;
+            const int jr = (int)(rg % BK);
+            const float *src = XB + (rg / BK) * (int64_t)(2 * DA * BK) + (jr >> 1) * (2 * DA) + (jr & 1);
 #pragma unroll
-            for (int q = 0; q < DM; q++) xrow[q] = valid ? src[q] : 0.0f;
+            for (int q = 0; q < DM; q++) xrow[q] = valid ? src[2 * q] : 0.0f;
         }
         const uint32_t lane_base = tmem + ((uint32_t)(sub * 32) << 16);
         if (h == 0) {
@@ -440,27 +441,37 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 // S = -r^2 from direct differences with the tile's x_j (broadcast loads)
                 const int xs = t % K::XS;
                 ptx::mbar_wait(&full_x[xs], (uint32_t)((t / K::XS) & 1));
-                // shared-space 128-bit loads (the aligned smem pointer is generic to the compiler)
-                const uint32_t xt = ptx::smem_u32(smem + xs * K::XB_BYTES) + (JW * h) * DA * 4;
+                // two points at a time on the paired FP32 pipe (FADD2 / FFMA2): the tile stores
+                // (x_j0q, x_j1q) adjacent, so one 128-bit shared load gives two packed pairs
+                const uint32_t xt = ptx::smem_u32(smem + xs * K::XB_BYTES) + (JW * h / 2) * (2 * DA) * 4;
+                unsigned long long xr2[DM];
 #pragma unroll
-                for (int jj = 0; jj < JW; jj++) {
-                    float r4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                for (int q = 0; q < DM; q++)
+                    asm("mov.b64 %0, {%1, %1};" : "=l"(xr2[q]) : "f"(xrow[q]));
 #pragma unroll
-                    for (int q4 = 0; q4 < (DM + 3) / 4; q4++) {
-                        float x[4];
-                        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
-                                     : "r"(xt + (jj * DA + 4 * q4) * 4));
+                for (int jp = 0; jp < JW / 2; jp++) {
+                    unsigned long long acc2[2] = {0ull, 0ull};
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int q = 4 * q4 + u;
+                    for (int q2 = 0; q2 < (DM + 1) / 2; q2++) {
+                        unsigned long long x2[2];
+                        asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];"
+                                     : "=l"(x2[0]), "=l"(x2[1])
+                                     : "r"(xt + (jp * 2 * DA + 4 * q2) * 4));
+#pragma unroll
+                        for (int u = 0; u < 2; u++) {
+                            const int q = 2 * q2 + u;
                             if (q < DM) {
-                                const float df = xrow[q] - x[u];
-                                r4[u] = fmaf(df, df, r4[u]);
+                                unsigned long long df;
+                                asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(df) : "l"(xr2[q]), "l"(x2[u]));
+                                asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc2[u]) : "l"(df));
                             }
                         }
                     }
-                    sv[jj] = __float_as_uint(-((r4[0] + r4[1]) + (r4[2] + r4[3])));
+                    float a0, a1, b0, b1;
+                    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2[0]));
+                    asm("mov.b64 {%0, %1}, %2;" : "=f"(b0), "=f"(b1) : "l"(acc2[1]));
+                    sv[2 * jp] = __float_as_uint(-(a0 + b0));
+                    sv[2 * jp + 1] = __float_as_uint(-(a1 + b1));
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&free_x[xs]);
@@ -545,8 +556,9 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
                 else if (q == d + 1) { a = 1.0f; b = e; }
             }
             Xa[j * DA + q] = a;
-            if (plain) {   // MODE 2: x_j as fp32 rows [BK][DA] of its tile, zero past d
-                XB[(j / BK) * (int64_t)(2 * DA * BK) + (j % BK) * DA + q] =
+            if (plain) {   // MODE 2: x_j fp32, point pairs interleaved: [BK/2][DA][2], zero past d
+                const int jj = (int)(j % BK);
+                XB[(j / BK) * (int64_t)(2 * DA * BK) + (jj >> 1) * (2 * DA) + 2 * q + (jj & 1)] =
                     (ok && q < d) ? xs[q] : 0.0f;
                 continue;
             }
