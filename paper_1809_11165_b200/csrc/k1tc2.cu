@@ -389,8 +389,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 const float sj = __uint_as_float(sv[4 * u + v]);
                 float kv;
                 if (MODE == 2) {
-                    // S = -rh^2 (clamped at 0 near the diagonal)
-                    const float rs2 = fmaxf(-sj, 0.0f);
+                    // sv holds +rh^2 (a sum of squares: no clamp needed)
+                    const float rs2 = sj;
                     const float rh = sqrt_approx(rs2);
                     kv = fmaf(rs2, 0.33333333333333333f, rh + 1.0f) *
                          ex2_approx(-1.4426950408889634f * rh);
@@ -470,8 +470,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     float a0, a1, b0, b1;
                     asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2[0]));
                     asm("mov.b64 {%0, %1}, %2;" : "=f"(b0), "=f"(b1) : "l"(acc2[1]));
-                    sv[2 * jp] = __float_as_uint(-(a0 + b0));
-                    sv[2 * jp + 1] = __float_as_uint(-(a1 + b1));
+                    sv[2 * jp] = __float_as_uint(a0 + b0);
+                    sv[2 * jp + 1] = __float_as_uint(a1 + b1);
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&free_x[xs]);
