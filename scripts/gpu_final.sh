@@ -10,5 +10,5 @@ timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/b
 for C in C1 C2 C3; do timeout 900 python bench.py --config $C --no-cpu-baseline > gpurun_out/bench_$C.json 2> gpurun_out/bench_$C.err; tail -c 300 gpurun_out/bench_$C.json; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1; tail -1 gpurun_out/launches_bench.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1tc2_rbf -c 1 -o gpurun_out/k1tc2_C3 python scripts/prof_matmul.py 200000 2 C3 > gpurun_out/prof_c3.log 2>&1; tail -1 gpurun_out/prof_c3.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1tc2_rbf -c 1 -o gpurun_out/k1tc2_C2m python scripts/prof_matmul.py 45730 3 C2 > gpurun_out/prof_c2m.log 2>&1; tail -1 gpurun_out/prof_c2m.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1tc2_rbf -c 1 -o gpurun_out/k1tc2_C2m python scripts/prof_matmul.py 45730 2 C2 > gpurun_out/prof_c2m.log 2>&1; tail -1 gpurun_out/prof_c2m.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_deriv_tc -c 1 -o gpurun_out/deriv_tc_C3 python scripts/prof_mll.py C3 > gpurun_out/prof_dtc.log 2>&1; tail -1 gpurun_out/prof_dtc.log
