@@ -167,18 +167,57 @@ k_LtR2(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
         for (int u = 0; u < 4; u++) acc[j][u] = 0.0;
     const int64_t i_beg = (int64_t)blockIdx.x * rows_per_blk;
     const int64_t i_end = min(nloc, i_beg + rows_per_blk);
+    // The next chunk's L / R values are loaded into registers while the current chunk is
+    // multiplied (one chunk of loads in flight per thread instead of none): up to
+    // kPF elements per thread, else the loads are issued just before the stores.
+    constexpr int kPF = MPT <= 4 ? 24 : 0;
+    double lr[kPF > 0 ? kPF : 1];
+    const int nl = (k * KT + 255) / 256, nr = (KT * c + 255) / 256;
+    const bool pf = kPF > 0 && nl + nr <= kPF;
+    // fully unrolled over kPF with runtime predicates, so lr[] stays in registers
+    auto fetch = [&](int64_t i0, double *dst) {
+        const int rows = (int)min((int64_t)KT, i_end - i0);
+#pragma unroll
+        for (int q = 0; q < (kPF > 0 ? kPF : 1); q++) {
+            double v = 0.0;
+            if (q < nl) {
+                const int e = threadIdx.x + 256 * q;
+                const int m = e / KT, kk = e - m * KT;
+                if (e < k * KT && kk < rows) v = L[(int64_t)m * n + r0 + i0 + kk];
+            } else if (q < nl + nr) {
+                const int e = threadIdx.x + 256 * (q - nl);
+                if (e < KT * c && e / c < rows) v = R[i0 * c + e];
+            }
+            dst[q] = v;
+        }
+    };
+    if (pf && i_beg < i_end) fetch(i_beg, lr);
     for (int64_t i0 = i_beg; i0 < i_end; i0 += KT) {
         const int rows = (int)min((int64_t)KT, i_end - i0);
         __syncthreads();
-        for (int e = threadIdx.x; e < k * KT; e += 256) {
-            const int m = e / KT, kk = e - m * KT;
-            Lt[kk * k + m] = kk < rows ? L[(int64_t)m * n + r0 + i0 + kk] : 0.0;
-        }
-        for (int e = threadIdx.x; e < KT * c; e += 256) {
-            const int kk = e / c;
-            Rt[e] = kk < rows ? R[i0 * c + e] : 0.0;
+        if (pf) {
+#pragma unroll
+            for (int q = 0; q < (kPF > 0 ? kPF : 1); q++) {
+                if (q < nl) {
+                    const int e = threadIdx.x + 256 * q;
+                    if (e < k * KT) Lt[(e % KT) * k + e / KT] = lr[q];
+                } else if (q < nl + nr) {
+                    const int e = threadIdx.x + 256 * (q - nl);
+                    if (e < KT * c) Rt[e] = lr[q];
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < k * KT; e += 256) {
+                const int m = e / KT, kk = e - m * KT;
+                Lt[kk * k + m] = kk < rows ? L[(int64_t)m * n + r0 + i0 + kk] : 0.0;
+            }
+            for (int e = threadIdx.x; e < KT * c; e += 256) {
+                const int kk = e / c;
+                Rt[e] = kk < rows ? R[i0 * c + e] : 0.0;
+            }
         }
         __syncthreads();
+        if (pf && i0 + KT < i_end) fetch(i0 + KT, lr);
         if (act) {
             for (int kk = 0; kk < KT; kk++) {
                 double r[4];
