@@ -26,7 +26,11 @@ namespace bbmm {
 namespace dtc {
 
 constexpr int BM = 128, BK = 128;
-constexpr int NCW = 8;                         // compute warps
+#ifndef BBMM_DTC_NCW
+#define BBMM_DTC_NCW 8
+#endif
+constexpr int NCW = BBMM_DTC_NCW;              // compute warps (4 or 8)
+constexpr int JPW = BK / (NCW / 4);            // points of a tile per compute warp
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 constexpr int NBUF = 2;                        // TMEM W buffers (128 fp32 columns each)
@@ -186,12 +190,12 @@ k_deriv_tc(const float *__restrict__ Xs, const float *__restrict__ A32, int csa,
             ptx::tc_fence_after();
             const float *xj = reinterpret_cast<const float *>(smem + st * K::STAGE + K::WB_BYTES);
 #pragma unroll 1
-            for (int quarter = 0; quarter < 4; quarter++) {
+            for (int quarter = 0; quarter < JPW / 16; quarter++) {
                 // fp32 sums over 16 pairs, then folded into fp64 (as k7_deriv's FOLD = 16)
                 float acc[D + 1];
 #pragma unroll
                 for (int q = 0; q <= D; q++) acc[q] = 0.0f;
-                const int jb = h * 64 + quarter * 16;
+                const int jb = h * JPW + quarter * 16;
                 uint32_t wv[16];
                 ptx::tmem_ld16(lane_base + b * BK + jb, wv);
                 ptx::tmem_ld_wait();
