@@ -399,7 +399,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 }
                 // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
                 // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
-                if (MODE == 1) kv *= fmaxf(-1.3862943611198906f * sj, 0.0f);
+                // (the factor 2 ln 2 is applied in the epilogue: k~ (-S) <= 0.53 here)
+                if (MODE == 1) kv *= fmaxf(-sj, 0.0f);
                 // q = 2 + k~ in [2, 3]: exponent 128 (low bit 0), so the three low
                 // bytes are exactly the 22-bit fixed-point k~ 2^22 (round to nearest)
                 q[v] = __float_as_uint(kv + 2.0f);
@@ -512,7 +513,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
             double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * CS;
-            const double base = s * (ND == 4 ? 0x1p-52 : 0x1p-60);
+            const double base = s * (ND == 4 ? 0x1p-52 : 0x1p-60) *
+                                (MODE == 1 ? 1.3862943611198906 : 1.0);   // MODE 1: r^2 = -2 ln2 S
             const double cacc = acc_sm[C][rl];
 #pragma unroll
             for (int c = 0; c < C; c++) out[c] = base * Sc[c] * (acc_sm[c][rl] - cacc);
