@@ -389,11 +389,12 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 const float sj = __uint_as_float(sv[4 * u + v]);
                 float kv;
                 if (MODE == 2) {
-                    // sv holds +rh^2 (a sum of squares: no clamp needed)
+                    // sv holds +rh'^2 with rh' = log2(e) rh (a sum of squares: no clamp);
+                    // k~ = (1 + rh + rh^2/3) 2^(-rh') with rh = ln2 rh'
                     const float rs2 = sj;
                     const float rh = sqrt_approx(rs2);
-                    kv = fmaf(rs2, 0.33333333333333333f, rh + 1.0f) *
-                         ex2_approx(-1.4426950408889634f * rh);
+                    kv = fmaf(rs2, 0.16015100463940046f /* ln2^2 / 3 */,
+                              fmaf(rh, 0.69314718055994531f, 1.0f)) * ex2_approx(-rh);
                 } else {
                     kv = ex2_approx(sj);
                 }
@@ -604,8 +605,10 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
     double *mean = (double *)ctx->ws.get("tc_mean", kMaxDim * 8);
     float *sc_d = (float *)ctx->ws.get("tc_scale", kMaxDim * 4);
     float sc[kMaxDim];
-    // RBF: S = -|xs_i - xs_j|^2 = -(log2 e / 2) r^2 -> k~ = 2^S;  Matern: S = -5 r^2 = -rh^2
-    const double base = h.kind == BBMM_RBF ? std::sqrt(0.5 / std::log(2.0)) : std::sqrt(5.0);
+    // RBF: S = -|xs_i - xs_j|^2 = -(log2 e / 2) r^2 -> k~ = 2^S;  Matern: |xs_i - xs_j|^2 = rh'^2
+    // Matern: inputs scaled by sqrt5 log2(e) / l, so rh' = log2(e) rh feeds ex2 directly
+    const double base = h.kind == BBMM_RBF ? std::sqrt(0.5 / std::log(2.0))
+                                           : std::sqrt(5.0) / std::log(2.0);
     for (int q = 0; q < d; q++) sc[q] = (float)(base / h.ls[h.n_ls == 1 ? 0 : q]);
     BBMM_CUDA(cudaMemcpyAsync(sc_d, sc, sizeof(float) * d, cudaMemcpyHostToDevice, ctx->stream));
     k1tc_col_mean(ctx, X, n, d, mean);
@@ -720,7 +723,8 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         // The expanded distance 2 xs_i.xs_j - |xs_i|^2 - |xs_j|^2 loses ~eps32 max|xs|^2
         // absolutely; beyond max|xs|^2 = 16 (kernel-value error > ~1e-6) fall back to
         // the direct-difference FP64ACC path.
-        if (!(max_sq <= 16.0f)) return op;
+        // (Matern computes direct differences: no expanded-form error, no guard)
+        if (h.kind == BBMM_RBF && !(max_sq <= 16.0f)) return op;
         op.version = 2;
         op.kind = h.kind;
         op.nd = h.kind == BBMM_MATERN52 ? 5 : 4;
