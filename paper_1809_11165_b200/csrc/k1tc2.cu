@@ -1,25 +1,29 @@
-// k1tc2.cu -- Blackwell tensor-core kernel-matmul, version 2 (K1-TC2).
+// k1tc2.cu -- Blackwell tensor-core kernel-matmul (K1-TC): V = s K~ D on the fly.
 //
-// Same exact int8 contraction as k1tc.cu (DESIGN.md "K1-TC exact
-// contraction"), but with both operand streams that limited version 1 (the
-// shared-memory pipe: x_j broadcasts, A-tile stores, A reads by the MMA)
-// moved into tensor memory:
-//   * the exponent S_ij = -|xs_i - xs_j|^2 is itself a tcgen05 MMA (kind::tf32,
-//     "3xTF32" split for fp32-level accuracy) of augmented vectors
-//       A_i = [2 xs_i, -|xs_i|^2, 1],  B_j = [xs_j, 1, -|xs_j|^2]
-//     with A resident in TMEM for the CTA's rows and B_j streamed per tile;
-//     S lands in TMEM and is read with one tcgen05.ld per 32 j;
-//   * the int8 slices of the quantised kernel values are written straight
-//     to TMEM (tcgen05.st) and consumed as the A operand of the int8 MMAs.
-// Per pair a compute thread then issues ~5 instructions (ex2, 1 FFMA,
-// byte permutes) so the kernel is bound by the MUFU ex2 pipe.
+// The exact int8 contraction of DESIGN.md §6: kernel values k~ in [0, 1] as
+// 22-bit fixed point in three u8 slices (the low bytes of the fp32 q = 2 + k~),
+// D as 31-bit (RBF) or 39-bit (Matern) fixed point per column (k1tc.cu), all
+// slice products on the int8 tensor cores with exact integer accumulation in
+// TMEM, drained to fp64.  Per 128 x 128 tile:
+//   * RBF (MODE 0 / 1): the exponent S_ij = -|xs_i - xs_j|^2 is itself a
+//     tcgen05 MMA (kind::tf32, 3xTF32 split) of augmented vectors
+//       A_i = [2 xs_i, -|xs_i|^2, 1] (shared memory),  B_j = [xs_j, 1, -|xs_j|^2]
+//     (streamed [hi | lo] tiles) into a TMEM buffer; compute warps tcgen05.ld S,
+//     run ex2 on the MUFU (MODE 1: times r^2, the isotropic lengthscale
+//     derivative), quantise, and tcgen05.st the A slices over their S columns;
+//   * Matern-5/2 (MODE 2): distances from direct fp32 differences of x tiles
+//     streamed through the same ring (two points per FADD2 / FFMA2), then
+//     sqrt + ex2 on the MUFU -- the expanded form's ~1e-7 error breaks the
+//     parity bars for Matern.
+// The int8 MMAs read the A slices from TMEM and the packed D slices from
+// shared memory.
 //
-// CTA = 128 rows, 1 CTA per SM, 26 warps:
-//   warps 0-23: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
-//               h = w / 4 (16 of the 96 j) of every j tile
-//   warp 24   : producer (bulk copies of the B' distance tile and the packed
-//               D slices)
-//   warp 25   : MMA issuer: int8 contraction of tile t, then the distance
+// CTA = 128 rows, 1 CTA per SM, 18 warps:
+//   warps 0-15: compute; warp w serves TMEM lanes 32 (w % 4).. and the j-group
+//               h = w / 4 (32 of the 128 j) of every tile
+//   warp 16   : producer (bulk copies of the distance / x tile and the packed
+//               D slices, two rings)
+//   warp 17   : MMA issuer: int8 contraction of tile t, then the distance
 //               MMA of tile t + NBUF into the TMEM buffer just consumed
 #include <algorithm>
 #include <cmath>
