@@ -567,6 +567,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                    k > 0 ? k_used : 0, c, max_iter, tol};
         MbcgOut o;
         o.Z0 = Z0;
+        o.defer_host = true;                 // mbcg_finish after the final sync below
         mbcg_run(ctx, a, B, c, cholC, o);
         Timer t_cg(sm);
 
@@ -661,6 +662,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         BBMM_CUDA(cudaMemcpyAsync(hs, scal, 2 * 8, cudaMemcpyDeviceToHost, sm));
         BBMM_CUDA(cudaMemcpyAsync(&st_h, status, sizeof(int), cudaMemcpyDeviceToHost, sm));
         BBMM_CUDA(cudaStreamSynchronize(sm));
+        mbcg_finish(ctx, o);                 // mBCG host results + breakdown check (throws first)
         if (st_h) throw Error{BBMM_ERR_NUMERIC, "non-positive Ritz value in SLQ (Khat not PD?)"};
         const double logdet = hs[0] + hs[1];
         const double quad_y = hred[nq + 0], uu = hred[nq + 1], uz = hred[nq + 2];

@@ -246,6 +246,13 @@ struct MbcgOut {
     int iters_run = 0;
     float ms_matmul = 0.f;
     int matmul_launches = 0;
+    // defer_host: mbcg_run returns without the host copies / stream sync; the caller runs
+    // mbcg_finish after its own synchronisation (alpha, beta, relres, iters, ms_matmul and the
+    // breakdown check are valid only after that)
+    bool defer_host = false;
+    const double *rhist_d_ = nullptr;
+    int c_ = 0, max_iter_ = 0;
+    std::vector<cudaEvent_t> mm_ev_;
 };
 void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
                    double *cholC, double *logdet_d);
@@ -288,6 +295,7 @@ FusedPlan mbcg_fused_plan(bbmm_ctx_s *ctx, int64_t nloc, int c, int k, const dou
                           double *Cinv);
 void mbcg_fused_iteration(bbmm_ctx_s *ctx, const FusedPlan &p, const FusedIo &io);
 
+void mbcg_finish(bbmm_ctx_s *ctx, MbcgOut &out);
 void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
               const double *cholC, MbcgOut &out);
 void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, int kgen,

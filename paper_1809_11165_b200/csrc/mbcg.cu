@@ -976,30 +976,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         k_copy_U<<<256, 256, 0, sm>>>(U, nloc, c, out.U, out.ldu);
         launches++;
     }
-    MbcgState st_h;
-    out.alpha.assign((size_t)a.max_iter * c, 0.0);
-    out.beta.assign((size_t)a.max_iter * c, 0.0);
-    out.relres_hist.assign((size_t)a.max_iter * c, 0.0);
-    BBMM_CUDA(cudaMemcpyAsync(out.relres_hist.data(), rhist, (size_t)a.max_iter * c * 8,
-                              cudaMemcpyDeviceToHost, sm));
-    BBMM_CUDA(cudaMemcpyAsync(out.alpha.data(), ahist, (size_t)a.max_iter * c * 8,
-                              cudaMemcpyDeviceToHost, sm));
-    BBMM_CUDA(cudaMemcpyAsync(out.beta.data(), bhist, (size_t)a.max_iter * c * 8,
-                              cudaMemcpyDeviceToHost, sm));
-    BBMM_CUDA(cudaMemcpyAsync(&st_h, st, sizeof(MbcgState), cudaMemcpyDeviceToHost, sm));
-    BBMM_CUDA(cudaStreamSynchronize(sm));
-    BBMM_LAUNCH_CHECK();
-    float ms_tot = 0.f;
-    for (size_t q = 0; q + 1 < mm_ev.size(); q += 2) {
-        float ms = 0.f;
-        BBMM_CUDA(cudaEventElapsedTime(&ms, mm_ev[q], mm_ev[q + 1]));
-        ms_tot += ms;
-        cudaEventDestroy(mm_ev[q]);
-        cudaEventDestroy(mm_ev[q + 1]);
-    }
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    out.ms_matmul = ms_tot;
     out.matmul_launches = iters_run;
     out.iters_run = iters_run;
     out.U_d = U;
@@ -1007,10 +985,45 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     out.ahist_d = ahist;
     out.bhist_d = bhist;
     out.state_d = st;
+    out.rhist_d_ = rhist;
+    out.c_ = c;
+    out.max_iter_ = a.max_iter;
+    out.mm_ev_ = std::move(mm_ev);
+    ctx->launches += launches;   // matmul launches are counted by the matmul functions
+    // host-side results: now, or (defer_host) by the caller's mbcg_finish after its own
+    // stream synchronisation -- a latency-bound call then pays one host round trip less
+    if (!out.defer_host) mbcg_finish(ctx, out);
+}
+
+void mbcg_finish(bbmm_ctx_s *ctx, MbcgOut &out) {
+    cudaStream_t sm = ctx->stream;
+    const int c = out.c_, p = out.max_iter_;
+    MbcgState st_h;
+    out.alpha.assign((size_t)p * c, 0.0);
+    out.beta.assign((size_t)p * c, 0.0);
+    out.relres_hist.assign((size_t)p * c, 0.0);
+    BBMM_CUDA(cudaMemcpyAsync(out.relres_hist.data(), out.rhist_d_, (size_t)p * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaMemcpyAsync(out.alpha.data(), out.ahist_d, (size_t)p * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaMemcpyAsync(out.beta.data(), out.bhist_d, (size_t)p * c * 8,
+                              cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaMemcpyAsync(&st_h, out.state_d, sizeof(MbcgState), cudaMemcpyDeviceToHost, sm));
+    BBMM_CUDA(cudaStreamSynchronize(sm));
+    BBMM_LAUNCH_CHECK();
+    float ms_tot = 0.f;
+    for (size_t q = 0; q + 1 < out.mm_ev_.size(); q += 2) {
+        float ms = 0.f;
+        BBMM_CUDA(cudaEventElapsedTime(&ms, out.mm_ev_[q], out.mm_ev_[q + 1]));
+        ms_tot += ms;
+        cudaEventDestroy(out.mm_ev_[q]);
+        cudaEventDestroy(out.mm_ev_[q + 1]);
+    }
+    out.mm_ev_.clear();
+    out.ms_matmul = ms_tot;
     out.iters.assign(st_h.iters, st_h.iters + c);
     out.relres.assign(st_h.relres, st_h.relres + c);
     out.rho0.assign(st_h.rho0, st_h.rho0 + c);
-    ctx->launches += launches;   // matmul launches are counted by the matmul functions
     if (st_h.status != 0)
         throw Error{BBMM_ERR_NUMERIC,
                     "mBCG breakdown: alpha <= 0 or non-finite (operator not positive definite)"};
