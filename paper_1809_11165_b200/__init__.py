@@ -57,7 +57,8 @@ class Stats(C.Structure):
                 ("ms_pivchol", C.c_double), ("ms_mbcg", C.c_double), ("ms_matmul", C.c_double),
                 ("ms_slq", C.c_double), ("ms_deriv", C.c_double),
                 ("matmul_launches", C.c_int32), ("gpu_launches", C.c_int32),
-                ("matmul_path", C.c_int32), ("reserved_", C.c_int32)]
+                ("matmul_path", C.c_int32), ("unconverged", C.c_int32),
+                ("relres_max", C.c_double), ("ms_comm", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -233,10 +234,26 @@ def _dev(t, dtype, name, ctx):
     return _p(t.data_ptr())
 
 
+def _shape(t, shape, name):
+    """Sizes the C-ABI cannot check (it receives raw pointers): a wrong-sized array would make
+    the kernels read or write past the end of a device buffer.  None in `shape` = any size."""
+    got = tuple(t.shape)
+    if len(got) != len(shape) or any(w is not None and g != w for g, w in zip(got, shape)):
+        want = "x".join("*" if w is None else str(w) for w in shape)
+        raise ValueError(f"{name} must be {want}, got {'x'.join(map(str, got)) or 'scalar'}")
+
+
+def _X_shape(X, name="X"):
+    if X.dim() != 2:
+        raise ValueError(f"{name} must be n x d, got {tuple(X.shape)}")
+    return X.shape
+
+
 def kernel_matmul(ctx: Context, X, D, hyper: Hyper, kmode: int = ONTHEFLY):
     """V = (K(X,X) + sigma^2 I)[local rows] @ D.  X: n x d fp32, D: n x c fp64."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    _shape(D, (n, None), "D")
     c = D.shape[1]
     r0, r1 = ctx.local_rows(n)
     V = torch.empty((r1 - r0, c), dtype=torch.float64, device=X.device)
@@ -250,7 +267,7 @@ def kernel_matmul(ctx: Context, X, D, hyper: Hyper, kmode: int = ONTHEFLY):
 def pivchol(ctx: Context, X, hyper: Hyper, k: int):
     """Rank-k pivoted Cholesky of K_XX: (L [k x n fp64], pivots, k_used, resid_trace)."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
     L = torch.zeros((max(k, 1), n), dtype=torch.float64, device=X.device)
     piv = np.full(max(k, 1), -1, np.int64)
     ku, res = _i32(), _d()
@@ -265,9 +282,13 @@ def mbcg(ctx: Context, X, hyper: Hyper, B, L=None, max_iter: int = 20, tol: floa
          kmode: int = ONTHEFLY):
     """mBCG (Alg. S2) on Khat with preconditioner L L^T + sigma^2 I (L: k x n) or none."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    r0, r1 = ctx.local_rows(n)
+    _shape(B, (r1 - r0, None), "B (local rows x ncols)")
     nl, c = B.shape
     k = 0 if L is None else int(L.shape[0])
+    if L is not None:
+        _shape(L, (k, n), "L")
     U = torch.empty_like(B)
     al = np.zeros((max_iter, c))
     be = np.zeros((max_iter, c))
@@ -290,7 +311,10 @@ def mll_and_grad(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int
                  return_solves: bool = False):
     """One-call exact-GP marginal log likelihood and gradient (north-star entry)."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    _shape(y, (n,), "y")
+    if eps is not None:
+        _shape(eps, (n + k, t), "eps")
     nls = int(np.atleast_1d(hyper.log_ls).size)
     mll = _d()
     grad = np.zeros(nls + 2)
@@ -319,10 +343,10 @@ def predict(ctx: Context, X, y, Xstar, hyper: Hyper, k: int, max_iter: int = 20,
     """GP predictive mean and pointwise latent variance, Eq. 1 (bbmm_predict).
     Returns (mean, var) as fp64 cuda tensors of length nstar (var is None if variance=False)."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    _shape(y, (n,), "y")
+    _shape(Xstar, (None, d), "Xstar")
     ns = Xstar.shape[0]
-    if Xstar.dim() != 2 or Xstar.shape[1] != d:
-        raise ValueError("Xstar must be nstar x d")
     mean = torch.empty(ns, dtype=torch.float64, device=X.device)
     var = torch.empty(ns, dtype=torch.float64, device=X.device) if variance else None
     hp = hyper._c()
@@ -340,7 +364,8 @@ def train_adam(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int =
     """Adam hyperparameter training (bbmm_train_adam).
     Returns (trained Hyper, trace) with trace rows [mll(theta_s), theta_s...]."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    _shape(y, (n,), "y")
     nls = int(np.atleast_1d(hyper.log_ls).size)
     th = np.zeros(nls + 2)
     trace = np.zeros((max(steps, 1), nls + 3))
@@ -358,7 +383,10 @@ def sor_mbcg(ctx: Context, X, Xu, hyper: Hyper, B, k: int = 0, max_iter: int = 2
     """mBCG on the SoR / SGPR operator K_XU (K_UU + 1e-6 s I)^{-1} K_UX + sigma^2 I with a
     rank-k pivoted-Cholesky preconditioner of K_SoR (bbmm_sor_mbcg)."""
     torch = _torch()
-    n, d = X.shape
+    n, d = _X_shape(X)
+    _shape(Xu, (None, d), "Xu")
+    r0, r1 = ctx.local_rows(n)
+    _shape(B, (r1 - r0, None), "B (local rows x ncols)")
     m = Xu.shape[0]
     nl, c = B.shape
     U = torch.empty_like(B)

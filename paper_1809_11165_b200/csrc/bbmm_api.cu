@@ -68,20 +68,53 @@ Hyper make_hyper(const bbmm_hyper_t *hp, int d) {
 }
 
 // ------------------------------------------------------------------ comm
+namespace {
+struct CommSpan {   // pool events bracketing one collective on the context stream
+    bbmm_ctx_s *ctx;
+    explicit CommSpan(bbmm_ctx_s *c) : ctx(c) { record(); }
+    ~CommSpan() {
+        try { record(); } catch (...) {}
+    }
+    void record() {
+        if (ctx->n_comm_ev >= ctx->comm_events.size()) {
+            cudaEvent_t e;
+            BBMM_CUDA(cudaEventCreate(&e));
+            ctx->comm_events.push_back(e);
+        }
+        BBMM_CUDA(cudaEventRecord(ctx->comm_events[ctx->n_comm_ev++], ctx->stream));
+    }
+};
+}  // namespace
+
+void comm_timing_reset(bbmm_ctx_s *ctx) { ctx->n_comm_ev = 0; }
+
+double comm_timing_ms(bbmm_ctx_s *ctx) {
+    double tot = 0.0;
+    for (size_t q = 0; q + 1 < ctx->n_comm_ev; q += 2) {
+        float ms = 0.f;
+        BBMM_CUDA(cudaEventElapsedTime(&ms, ctx->comm_events[q], ctx->comm_events[q + 1]));
+        tot += ms;
+    }
+    return tot;
+}
+
 void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count) {
-    if (ctx->nranks <= 1) return;
+    if (!has_comm(ctx)) return;
+    CommSpan span(ctx);
     if (ctx->local) return local_allreduce_sum(ctx, buf, count);
     BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 
 void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count) {
-    if (ctx->nranks <= 1) return;
+    if (!has_comm(ctx)) return;
+    CommSpan span(ctx);
     if (ctx->local) return local_allreduce_max(ctx, buf, count);
     BBMM_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclMax, ctx->comm, ctx->stream));
 }
 
 void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank) {
-    if (ctx->nranks <= 1) return;
+    if (!has_comm(ctx)) return;
+    CommSpan span(ctx);
     if (ctx->local) return local_allgather(ctx, buf, bytes_per_rank);
     char *b = (char *)buf;
     BBMM_NCCL(ncclAllGather(b + (size_t)ctx->rank * bytes_per_rank, b, bytes_per_rank, ncclChar,
@@ -325,6 +358,8 @@ bbmm_status_t bbmm_ctx_destroy(bbmm_ctx_t ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->ws.release_all();
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
+    for (cudaEvent_t e : ctx->mm_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->comm_events) cudaEventDestroy(e);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -351,7 +386,8 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
         ctx->local = nullptr;
         ctx->nranks = nranks;
         ctx->rank = rank;
-        if (nranks > 1) {
+        // nranks == 1 with an id: a 1-rank communicator, every collective still issued
+        if (nranks > 1 || uid != nullptr) {
             BBMM_REQUIRE(uid != nullptr, "unique id is NULL");
             ncclUniqueId id;
             std::memcpy(&id, uid, sizeof(id));
@@ -530,6 +566,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         const int launches0 = ctx->launches;
         check_finite(ctx, X, n * d, "X");
         check_finite(ctx, y, n, "y");
+        comm_timing_reset(ctx);
         Timer t_start(sm);
         const int c = t + 1;
         RowRange rr = local_rows(ctx, n);
@@ -710,6 +747,14 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             s.matmul_launches = o.matmul_launches;
             s.gpu_launches = ctx->launches - launches0;
             s.matmul_path = tcop.version == 3 ? 3 : tcop.version == 2 ? 2 : (Kst ? 1 : 0);
+            s.relres_max = 0.0;
+            bool active = false;
+            for (int col = 0; col < c && col < (int)o.relres.size(); col++) {
+                s.relres_max = std::max(s.relres_max, o.relres[col]);
+                active |= tol > 0.0 && o.iters[col] >= max_iter && o.relres[col] >= tol;
+            }
+            s.unconverged = (active || s.relres_max >= kUnconvergedRelres) ? 1 : 0;
+            s.ms_comm = comm_timing_ms(ctx);
             *stats_h = s;
         }
         BBMM_CUDA(cudaStreamSynchronize(sm));

@@ -20,6 +20,9 @@ constexpr int kMaxInducing = 512;  // SoR operator: inducing points m (row f4)
 constexpr int kMaxRank = 128;    // preconditioner rank k
 constexpr int kMaxDim = 32;      // input dimension d
 constexpr int kNumSMs = 148;
+// bbmm_stats_t.unconverged: relres at exit above which mBCG counts as unconverged (SURVEY.md §8c
+// regime B; regime A runs end at <= 1e-6, the regime-B configs at 1e-2..0.2)
+constexpr double kUnconvergedRelres = 1e-3;
 
 // ---------------------------------------------------------------- status
 struct Error {
@@ -110,6 +113,13 @@ struct bbmm_ctx_s {
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
     int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
     bbmm::LocalGroup *local = nullptr;   // in-process rank group (comm_local.cu) instead of NCCL
+    // timing events of the mBCG matmuls, reused across calls (created on first use, destroyed
+    // with the context): no per-call event creation, nothing to leak when a call throws
+    std::vector<cudaEvent_t> mm_events;
+    // collective timing (bbmm_stats_t.ms_comm): event pairs around every collective since the
+    // last comm_timing_reset, reused across calls like mm_events
+    std::vector<cudaEvent_t> comm_events;
+    size_t n_comm_ev = 0;
 };
 
 namespace bbmm {
@@ -204,7 +214,7 @@ int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const dou
 bool k2tc_supported(int c);
 size_t k2tc_vpart_elems(int64_t n, int64_t nloc, int c);
 size_t k2tc_kq_bytes(int64_t n, int64_t nloc);
-void k2tc_build(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+void k2tc_build(bbmm_ctx_s *ctx, const float *X, int d, const Hyper &h, int64_t n, int64_t r0,
                 int64_t nloc, uint8_t *Kq);
 int k2tc_matmul(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const double *S, int c,
                 int64_t n, int64_t nloc, double s, double *Vpart, size_t cap, cudaEvent_t ev0,
@@ -252,8 +262,9 @@ struct MbcgOut {
     bool defer_host = false;
     const double *rhist_d_ = nullptr;
     int c_ = 0, max_iter_ = 0;
-    std::vector<cudaEvent_t> mm_ev_;
+    int n_ev_ = 0;   // ctx->mm_events[0, n_ev_) bracket the matmuls of this run (pairs)
 };
+cudaEvent_t mm_event(bbmm_ctx_s *ctx, size_t i);
 void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
                    double *cholC, double *logdet_d);
 // sor.cu: Bs = Lu^{-1} K_UX (m x n fp64, replicated), K_SoR = Bs^T Bs
@@ -321,7 +332,12 @@ int derivative_pass_tc(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64
 void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red);
 
 // ------------------------------------------------------------- comm
+// A context communicates when it has an NCCL communicator (also a 1-rank one, which issues
+// every collective as on G ranks) or an in-process rank group.
+inline bool has_comm(const bbmm_ctx_s *ctx) { return ctx->comm != nullptr || ctx->local != nullptr; }
 void allreduce_sum(bbmm_ctx_s *ctx, double *buf, size_t count);
 void allgather_rows(bbmm_ctx_s *ctx, void *buf, size_t bytes_per_rank);
+void comm_timing_reset(bbmm_ctx_s *ctx);
+double comm_timing_ms(bbmm_ctx_s *ctx);   // after a stream sync
 
 }  // namespace bbmm

@@ -13,22 +13,25 @@
 // 22-bit k~ as on the fly, measured 1.4e-4 solve error against the oracle at
 // the C2 shape, n = 3000: over the 1e-4 bar where mBCG is not converged.)  Every mBCG
 // iteration then streams the slices from HBM with bulk copies (TMA engine) and
-// contracts them with the packed search directions (k1tc.cu format with five
-// u8 slices p4..p0: D as 39-bit fixed point per column) on the int8 tensor
+// contracts them with the packed search directions (k1tc.cu format with seven
+// u8 slices p6..p0: D as 55-bit fixed point per column) on the int8 tensor
 // cores with exact uint32 accumulation in TMEM.  The kernel is bound by HBM
-// (4 n_loc n bytes per K D); the tensor work (20 slice products) is < 50 % of
-// the int8 pipe.  Why 39 bits of D (K1-TC uses 31): where mBCG is not yet
-// converged at p the iterates amplify per-iteration rounding of D -- an fp64
-// emulation at the C2 shape (n = 3000, p = 20) moves the solves by 1.3e-4
-// with 31-bit D and by 2.9e-6 with 39-bit D.
+// (4 n_loc n bytes per K D); the tensor work (28 slice products) stays below
+// the HBM time.  Why 55 bits of D (K1-TC uses 31): where mBCG is not yet
+// converged at p ("regime B") the iterates amplify per-iteration
+// rounding of D -- an fp64 emulation at the C2 shape (n = 3000, p = 20) moves the
+// solves by 1.3e-4 with 31-bit D and by 2.9e-6 with 39-bit D, and at n = 12 000
+// (relres 0.04) even 47-bit D moves them by 2.2e-4: 55 bits put the
+// rounding of D at the level of an fp64 product (2^-55 of the column maximum).
 //
 // CTA (persistent, one per SM, 192 threads):
 //   warps 0-3: epilogue -- drain a unit's accumulators (TMEM lane quarter w),
 //              fold the six weighted blocks into fp64, write Vpart
 //   warp 4   : producer -- bulk copies of the K-slice tile (32 KB) and the
 //              D-slice tile (NB x 64 B) of each 64-point stage
-//   warp 5   : MMA issuer -- 4 tcgen05.mma.kind::i8 (q3 .. q0 times the
-//              whole [p4|p3|p2|p1|p0] operand) per 32-point K-step
+//   warp 5   : MMA issuer -- tcgen05.mma.kind::i8 of q3 .. q0 times the
+//              [p6|..|p0] operand (one MMA per slice group of N <= 256) per
+//              32-point K-step
 // Work unit = (128-row block, j-split); a split never exceeds the uint32
 // accumulation window, so each unit is drained exactly once, into one of two
 // TMEM accumulator sets (the MMAs of unit u+1 overlap the drain of unit u).
@@ -46,12 +49,13 @@ namespace k2tc {
 constexpr int BM = 128;                    // rows per unit (TMEM lanes)
 constexpr int SK = 64;                     // j points per pipeline stage
 constexpr int NQ = 4;                      // K slices (30-bit fixed point)
-constexpr int ND = 5;                      // D slices (39-bit fixed point, k1tc_pack nd = 5)
+constexpr int ND = 7;                      // D slices (55-bit fixed point, k1tc_pack nd = 7)
 constexpr int SLICE_BYTES = BM * SK;       // one u8 slice of a tile: [SK/16][BM][16 B]
 constexpr int A_BYTES = NQ * SLICE_BYTES;  // q0 | q1 | q2 | q3
-// uint32 accumulation bound: block k collects q_a p_b with a + b = 7 - k; all
-// bytes <= 255, q3 <= 0x40, p4 <= 0x80, so the largest per-point block sum is
-// a + b = 3: 64*255 + 3*255*255 = 211395 -> < 20317 points per window.
+// uint32 accumulation bound: block k collects q_a p_b with a + b = NBLK - 1 - k
+// (at most NQ = 4 pairs); all bytes <= 255, q3 <= 0x40, p6 <= 0x80, so the
+// largest per-point block sum is 64*255 + 3*255*255 = 211395 -> < 20317 points
+// per window.
 constexpr int BLOCK_MAX = 211395;
 constexpr int WINDOW = (int)(4294967295ull / BLOCK_MAX) / SK * SK;
 static_assert((double)WINDOW * BLOCK_MAX < 4294967296.0, "uint32 window bound");
@@ -68,11 +72,11 @@ struct Cfg {
     static constexpr int C1 = C + 1;            // + constant offset column
     static_assert(C1 <= 48, "too many columns");
     static constexpr int BLK = (C1 + 15) & ~15; // N = ND BLK must be a multiple of 16
-    static constexpr int NB = ND * BLK;         // MMA N: [p4 | p3 | p2 | p1 | p0]
-    static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
+    static constexpr int NB = ND * BLK;         // B rows: [p6 | p5 | .. | p0]
+    static constexpr int G = (256 / BLK) < ND ? (256 / BLK) : ND;   // D slices per MMA (N <= 256)
+    static_assert((G * BLK) % 16 == 0 && ((ND % G) * BLK) % 16 == 0, "MMA N");
     static constexpr int NBLK = NQ + ND - 1;    // accumulator blocks
-    static constexpr int ACC_COLS = NBLK * BLK; // block k has weight 2^(8 (7 - k))
-    static_assert(NBLK == 8, "fold weights below assume 8 blocks");
+    static constexpr int ACC_COLS = NBLK * BLK; // block k has weight 2^(8 (NBLK - 1 - k))
     static constexpr int ACC_END = r32(ACC_COLS);
     static constexpr int NSET = 2 * ACC_END <= 512 ? 2 : 1;
     static constexpr int TMEM_COLS = pow2_cols(NSET * ACC_END);
@@ -87,27 +91,37 @@ struct Cfg {
 // --------------------------------------------------------------------------
 // Build: Kq tile (rb, t) = the four u8 slices of round(k~ 2^30) for rows
 // rb*128.. and points t*SK.. (zeros past n_loc / n), K-major core-matrix
-// layout [slice][SK/16 chunks][128 rows][16 B].  Thread = row; kernel values
-// from direct fp32 differences of the scaled inputs (same k~ map as K2).
+// layout [slice][SK/16 chunks][128 rows][16 B].  Thread = row.  The kernel
+// values are evaluated in fp64 from the fp32 inputs (the method's definition,
+// readings R1/R2: r^2 = sum_q ((x_iq - x_jq)/l_q)^2, k~ = exp(-r^2/2) or
+// (1 + sqrt5 r + 5r^2/3) exp(-sqrt5 r)), so the 2^-31 fixed-point rounding is
+// the only error of the stored operator: an fp32 distance alone perturbs K by
+// ~1e-7 relative, which an unconverged mBCG amplifies past the 1e-4 solve bar
+// (C2 full size: 4.1e-4 with fp32 distances).  K is built once
+// per call, so the fp64 work (about 60 DFMA-pipe ops per entry) is paid once,
+// not per iteration.
 // --------------------------------------------------------------------------
+struct InvLs {
+    double v[kMaxDim];   // 1 / l_q (ARD) or 1 / l repeated, 0 past d
+};
+
 template <int KIND, int D>
 __global__ void __launch_bounds__(BM)
-k_build_kq(const float *__restrict__ Xs, int64_t n, int64_t r0, int64_t nloc, int64_t ntiles,
-           uint8_t *__restrict__ Kq) {
-    constexpr int DS = round4(D);
-    __shared__ float xj_s[SK][DS];
+k_build_kq64(const float *__restrict__ X, int d, InvLs il, int64_t n, int64_t r0, int64_t nloc,
+             int64_t ntiles, uint8_t *__restrict__ Kq) {
+    __shared__ double xj_s[SK][D];
     const int64_t t = blockIdx.x, rb = blockIdx.y;
     const int rl = threadIdx.x;
     const int64_t i = rb * BM + rl;
-    for (int e = threadIdx.x; e < SK * DS; e += BM) {
-        const int jj = e / DS;
+    for (int e = threadIdx.x; e < SK * D; e += BM) {
+        const int jj = e / D, q = e % D;
         const int64_t j = t * SK + jj;
-        xj_s[jj][e % DS] = j < n ? Xs[j * DS + e % DS] : 0.0f;
+        xj_s[jj][q] = (j < n && q < d) ? (double)X[j * d + q] * il.v[q] : 0.0;
     }
-    float xi[D];
+    double xi[D];
     const bool vi = i < nloc;
 #pragma unroll
-    for (int q = 0; q < D; q++) xi[q] = vi ? Xs[(r0 + i) * DS + q] : 0.0f;
+    for (int q = 0; q < D; q++) xi[q] = (vi && q < d) ? (double)X[(r0 + i) * d + q] * il.v[q] : 0.0;
     __syncthreads();
     uint8_t *tile = Kq + (rb * ntiles + t) * (int64_t)A_BYTES;
 #pragma unroll 1
@@ -120,16 +134,24 @@ k_build_kq(const float *__restrict__ Xs, int64_t n, int64_t r0, int64_t nloc, in
             for (int v = 0; v < 4; v++) {
                 const int jj = ch * 16 + 4 * g + v;
                 const int64_t j = t * SK + jj;
-                float rs2 = 0.0f;
+                double r2 = 0.0;
 #pragma unroll
                 for (int qd = 0; qd < D; qd++) {
-                    const float df = xi[qd] - xj_s[jj][qd];
-                    rs2 = fmaf(df, df, rs2);
+                    const double df = xi[qd] - xj_s[jj][qd];
+                    r2 = fma(df, df, r2);
                 }
-                // K_ii = s exactly (rs2 = 0 -> k~ = 1 -> q = 2^30); k~ 2^30 keeps every bit
-                // of the fp32 value for k~ >= 2^-6 (and 2^-31 absolute below)
-                const float kv = (vi && j < n) ? kval_scaled<KIND>(r0 + i == j ? 0.0f : rs2) : 0.0f;
-                q[v] = __float2uint_rn(kv * 1073741824.0f);
+                double kv = 0.0;
+                if (vi && j < n) {
+                    if (r0 + i == j) {
+                        kv = 1.0;                        // K_ii = s exactly
+                    } else if (KIND == 0) {
+                        kv = exp(-0.5 * r2);
+                    } else {
+                        const double sr = sqrt(5.0 * r2);
+                        kv = (1.0 + sr + (5.0 / 3.0) * r2) * exp(-sr);
+                    }
+                }
+                q[v] = __double2uint_rn(kv * 1073741824.0);
             }
 #pragma unroll
             for (int a = 0; a < NQ; a++) {
@@ -148,7 +170,7 @@ k_build_kq(const float *__restrict__ Xs, int64_t n, int64_t r0, int64_t nloc, in
 }
 
 // --------------------------------------------------------------------------
-// V (split s of unit u) = s_out * S_c * sum_j k~_ij (P'_jc - 2^38) 2^-68
+// V (split s of unit u) = s_out * S_c * sum_j k~_ij (P'_jc - 2^54) 2^-84
 // --------------------------------------------------------------------------
 template <int C>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -206,7 +228,9 @@ k2tc_stored(const uint8_t *__restrict__ Kq, const uint8_t *__restrict__ Bpack,
         __syncwarp();
     } else if (warp == MMA_WARP) {
         // --------------------------------------------------------- MMA issuer
-        constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
+        constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::G * K::BLK, false, false);
+        constexpr int GR = ND % K::G;                 // slices of the last, partial group
+        constexpr uint32_t IDR = ptx::idesc_i8(BM, (GR ? GR : 1) * K::BLK, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         ptx::tc_fence_after();
@@ -227,14 +251,20 @@ k2tc_stored(const uint8_t *__restrict__ Kq, const uint8_t *__restrict__ Bpack,
                     const uint32_t sbb = sa + A_BYTES;
 #pragma unroll
                     for (int ks = 0; ks < SK / 32; ks++) {
-                        const uint64_t bd = ptx::smem_desc_kmajor(sbb + ks * 2 * K::NB * 16, K::NB * 16, 128);
+                        const uint32_t kb = sbb + ks * 2 * K::NB * 16;
                         const uint32_t ka = sa + ks * 2 * BM * 16;
-                        // q_a (weight 2^(8a)) times [p4|..|p0] -> blocks 3 - a .. 7 - a
+                        // q_a (weight 2^(8a)) times D-slice group [p_(ND-1-g0) ..] ->
+                        // blocks (NQ - 1 - a) + g0 ..
 #pragma unroll
-                        for (int a = NQ - 1; a >= 0; a--)
-                            ptx::mma_i8_ss(acc + (NQ - 1 - a) * K::BLK,
-                                           ptx::smem_desc_kmajor(ka + a * SLICE_BYTES, BM * 16, 128),
-                                           bd, IDQ, 1u);
+                        for (int a = NQ - 1; a >= 0; a--) {
+                            const uint64_t ad = ptx::smem_desc_kmajor(ka + a * SLICE_BYTES, BM * 16, 128);
+#pragma unroll
+                            for (int g0 = 0; g0 < ND; g0 += K::G)
+                                ptx::mma_i8_ss(acc + (NQ - 1 - a + g0) * K::BLK, ad,
+                                               ptx::smem_desc_kmajor(kb + g0 * K::BLK * 16,
+                                                                     K::NB * 16, 128),
+                                               g0 + K::G <= ND ? IDQ : IDR, 1u);
+                        }
                     }
                     ptx::mma_commit(&free_b[st]);
                 }
@@ -276,7 +306,7 @@ k2tc_stored(const uint8_t *__restrict__ Kq, const uint8_t *__restrict__ Bpack,
                 for (int e = 0; e < 32; e++) {
                     const int col = q0 + e, k = col / K::BLK, c = col % K::BLK;
                     if (col < K::ACC_COLS && c <= C)
-                        a[c] = fma(0x1p56 / (double)(1ull << (8 * k)), (double)v[e], a[c]);
+                        a[c] = fma(ldexp(1.0, 8 * (K::NBLK - 1 - k)), (double)v[e], a[c]);
                 }
             }
             // zero the set for its next unit, then hand it back to the issuer
@@ -292,7 +322,7 @@ k2tc_stored(const uint8_t *__restrict__ Kq, const uint8_t *__restrict__ Bpack,
             const int64_t row = rb * BM + warp * 32 + lane;
             if (row < nloc) {
                 double *out = Vpart + ((int64_t)split * nloc + row) * CS;
-                const double bs = s * 0x1p-68;
+                const double bs = s * 0x1p-84;     // 2^-30 (k~) x 2^-54 (D)
 #pragma unroll
                 for (int c = 0; c < C; c++) out[c] = bs * Sc[c] * (a[c] - a[C]);
 #pragma unroll
@@ -376,18 +406,21 @@ size_t k2tc_kq_bytes(int64_t n, int64_t nloc) {
            (size_t)k1tc_pad_rows(n) * k2tc::NQ;
 }
 
-void k2tc_build(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64_t n, int64_t r0,
+void k2tc_build(bbmm_ctx_s *ctx, const float *X, int d, const Hyper &h, int64_t n, int64_t r0,
                 int64_t nloc, uint8_t *Kq) {
     if (nloc <= 0) return;
     const int64_t npad = k1tc_pad_rows(n);
     const int64_t ntiles = npad / k2tc::SK;
     dim3 grid((unsigned)ntiles, (unsigned)ceil_div(nloc, k2tc::BM));
-    if (kind == BBMM_RBF) {
-        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq<0, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
-                                   Xs, n, r0, nloc, ntiles, Kq)))
+    k2tc::InvLs il{};
+    for (int q = 0; q < d; q++) il.v[q] = 1.0 / h.ls[h.n_ls == 1 ? 0 : q];
+    const int dp = pad_dim(d);
+    if (h.kind == BBMM_RBF) {
+        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq64<0, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
+                                   X, d, il, n, r0, nloc, ntiles, Kq)))
     } else {
-        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq<1, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
-                                   Xs, n, r0, nloc, ntiles, Kq)))
+        BBMM_DISPATCH_DIMS(dp, (k2tc::k_build_kq64<1, D_><<<grid, k2tc::BM, 0, ctx->stream>>>(
+                                   X, d, il, n, r0, nloc, ntiles, Kq)))
     }
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
@@ -401,7 +434,7 @@ TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const f
     TcOperand op;
     if (ctx->matmul_tc && k2tc_supported(c)) {
         uint8_t *kq = (uint8_t *)ctx->ws.get("Kq", k2tc_kq_bytes(n, nloc));
-        k2tc_build(ctx, h.kind, Xs, dp, n, r0, nloc, kq);
+        k2tc_build(ctx, X, d, h, n, r0, nloc, kq);
         op.version = 3;
         op.d = d;
         op.kind = h.kind;

@@ -706,6 +706,15 @@ void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, i
     ctx->launches++;
 }
 
+cudaEvent_t mm_event(bbmm_ctx_s *ctx, size_t i) {
+    while (ctx->mm_events.size() <= i) {
+        cudaEvent_t e;
+        BBMM_CUDA(cudaEventCreate(&e));
+        ctx->mm_events.push_back(e);
+    }
+    return ctx->mm_events[i];
+}
+
 void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
               const double *cholC, MbcgOut &out) {
     const int c = a.c, k = a.k;
@@ -755,7 +764,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     if (smem_S > 48 * 1024)
         BBMM_CUDA(cudaFuncSetAttribute(k_precond_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem_S));
-    const bool multi = ctx->nranks > 1;
+    const bool multi = has_comm(ctx);
     int launches = 0;
 
     auto reduce = [&](int m, double *dst) {
@@ -905,21 +914,13 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     }
 
     // ---------------- iterations
-    cudaEvent_t ev0, ev1;
-    BBMM_CUDA(cudaEventCreate(&ev0));
-    BBMM_CUDA(cudaEventCreate(&ev1));
-    std::vector<cudaEvent_t> mm_ev;
     // pinned flag for convergence polling, allocated once per context and only when needed
     // (cudaMallocHost costs tens of ms; with tol == 0 nothing is polled)
     if (a.tol > 0.0 && !ctx->pinned_flag) BBMM_CUDA(cudaMallocHost(&ctx->pinned_flag, sizeof(int)));
     int *any_h = ctx->pinned_flag;
     int iters_run = 0;
     for (int j = 0; j < a.max_iter; j++) {
-        cudaEvent_t e0, e1;
-        BBMM_CUDA(cudaEventCreate(&e0));
-        BBMM_CUDA(cudaEventCreate(&e1));
-        mm_ev.push_back(e0);
-        mm_ev.push_back(e1);
+        cudaEvent_t e0 = mm_event(ctx, 2 * (size_t)j), e1 = mm_event(ctx, 2 * (size_t)j + 1);
         int splits;
         if (use_sor)
             splits = sor_matmul(e0, e1);
@@ -976,8 +977,6 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         k_copy_U<<<256, 256, 0, sm>>>(U, nloc, c, out.U, out.ldu);
         launches++;
     }
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
     out.matmul_launches = iters_run;
     out.iters_run = iters_run;
     out.U_d = U;
@@ -988,7 +987,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     out.rhist_d_ = rhist;
     out.c_ = c;
     out.max_iter_ = a.max_iter;
-    out.mm_ev_ = std::move(mm_ev);
+    out.n_ev_ = 2 * iters_run;
     ctx->launches += launches;   // matmul launches are counted by the matmul functions
     // host-side results: now, or (defer_host) by the caller's mbcg_finish after its own
     // stream synchronisation -- a latency-bound call then pays one host round trip less
@@ -1012,14 +1011,12 @@ void mbcg_finish(bbmm_ctx_s *ctx, MbcgOut &out) {
     BBMM_CUDA(cudaStreamSynchronize(sm));
     BBMM_LAUNCH_CHECK();
     float ms_tot = 0.f;
-    for (size_t q = 0; q + 1 < out.mm_ev_.size(); q += 2) {
+    for (int q = 0; q + 1 < out.n_ev_; q += 2) {
         float ms = 0.f;
-        BBMM_CUDA(cudaEventElapsedTime(&ms, out.mm_ev_[q], out.mm_ev_[q + 1]));
+        BBMM_CUDA(cudaEventElapsedTime(&ms, ctx->mm_events[q], ctx->mm_events[q + 1]));
         ms_tot += ms;
-        cudaEventDestroy(out.mm_ev_[q]);
-        cudaEventDestroy(out.mm_ev_[q + 1]);
     }
-    out.mm_ev_.clear();
+    out.n_ev_ = 0;
     out.ms_matmul = ms_tot;
     out.iters.assign(st_h.iters, st_h.iters + c);
     out.relres.assign(st_h.relres, st_h.relres + c);
