@@ -35,9 +35,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LARGE = os.path.join(HERE, "golden", "large")
 OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
 
-# (name, n, bars for solve / grad where the oracle is unconverged at p (regime B))
 CASES = [("C4", 131072), ("C3", 80000), ("C2", 45730)]
-REGIME_B_BARS = {"solve": 1e-3, "grad": 5e-3}
+# Regime B: the solve bar is twice the oracle's own rounding floor -- how far the
+# fp64 oracle's solves move when its right-hand side moves by one ulp (<name>_n<n>_floor.json,
+# scripts/oracle_rounding_floor.py) -- and at least the north-star 1e-4; the gradient bar is 5x the
+# regime-A bar (the gradient contracts the same unconverged solves).
+REGIME_B_GRAD = 5e-3
+
+
+def _regime_b_solve_bar(name, n):
+    path = os.path.join(LARGE, f"{name}_n{n}_floor.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} missing (scripts/oracle_rounding_floor.py {name}:{n})")
+    return max(1e-4, 2.0 * json.load(open(path))["solve_floor_max"])
 
 
 def _load(name, n):
@@ -80,8 +90,9 @@ def _run(ctx, name, n, prec):
         ctx.set_matmul_precision(bb.INT8EXACT)
     U = g["U"].cpu().numpy()
     Uo = z["U"].astype(np.float64)
+    cols = np.linalg.norm(U - Uo, axis=0) / z["Unorm"]
     err = dict(
-        solve=float((np.linalg.norm(U - Uo, axis=0) / z["Unorm"]).max()),
+        solve=float(cols.max()), solve_y=float(cols[0]), solve_probe_median=float(np.median(cols[1:])),
         logdet=float(abs(g["stats"]["logdet"] - float(z["logdet"])) / abs(float(z["logdet"]))),
         mll=float(abs(g["mll"] - float(z["mll"])) / abs(float(z["mll"]))),
         grad=float(np.linalg.norm(g["grad"] - z["grad"]) / np.linalg.norm(z["grad"])),
@@ -109,11 +120,11 @@ def test_fullsize_mll_and_grad_matches_cached_oracle(ctx, name, n):
         assert g["stats"]["unconverged"] == 0
     else:
         assert g["stats"]["unconverged"] == 1
-        assert err["solve"] <= REGIME_B_BARS["solve"], err
-        assert err["grad"] <= REGIME_B_BARS["grad"], err
+        assert err["solve"] <= _regime_b_solve_bar(name, n), err
+        assert err["grad"] <= REGIME_B_GRAD, err
 
 
-@pytest.mark.parametrize("name,n", [c for c in CASES if c[0] != "C4"])
+@pytest.mark.parametrize("name,n", CASES)
 def test_fullsize_fp64acc_reference_point(ctx, name, n):
     """The CUDA-core fp64-accumulating operator on the same cached cases: the floor an fp32
     kernel value with fp64 D reaches (DESIGN.md §6a compares the default path against it)."""
