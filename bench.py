@@ -41,6 +41,17 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+# what the K^D arithmetic is, per operator (matmul_path of bbmm_stats_t)
+DTYPE = {
+    0: "fp32 kernel values x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
+    1: "stored fp32 K x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
+    2: "22-bit fixed-point k~ (3 u8 slices) x 31-bit fixed-point D (4 u8 slices), exact int32 "
+       "accumulation on tcgen05; fp64 CG",
+    3: "stored 30-bit fixed-point K (4 u8 slices, fp64-built) x 55-bit fixed-point D (7 u8 slices), "
+       "exact int32 accumulation on tcgen05; fp64 CG",
+}
+
+
 def work_per_matmul(cfg):
     """Algorithmic work of one Khat*D: n^2 kernel
     evaluations (one ex2 each for RBF; ex2 + sqrt for Matern) and 2 n^2 c
@@ -180,6 +191,9 @@ def main():
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
+        # NCCL's own communicator lines (transport, NVLS / P2P channels) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import paper_1809_11165_b200 as bb
@@ -298,16 +312,6 @@ def main():
                     "peak_source": f"hbm_gbs of MEASURED_PEAKS.json ({src})",
                     "kernel_ms": mm_ms,
                     "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
-    elif path == 2 and tensor_frac(cfg, world, mm_ms, pk) > achieved / peak_exp:
-        # K1-TC where the tensor pipe, not the MUFU, binds (large d / many columns: C3)
-        tf, tach, tpk = tensor_frac(cfg, world, mm_ms, pk, detail=True)
-        roofline = {"bound": "tensor", "kernel": kname, "achieved": tach, "peak": tpk,
-                    "unit": "TFLOP/s (dense-bf16 equivalent)", "frac": tf, "traffic": traffic,
-                    "peak_source": "bf16_tflops of MEASURED_PEAKS.json; tf32 work counted x2 and "
-                                   "int8 work x0.5 (nominal B200 dense rates 1.1 / 2.25 / 4.5 "
-                                   "PFLOP/s, B200_PROFILING.md)",
-                    "mufu_frac": achieved / peak_exp, "kernel_ms": mm_ms,
-                    "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
     else:
         roofline = {"bound": "alu", "kernel": kname, "achieved": achieved,
                     "peak": peak_exp, "unit": "Gop/s (MUFU ex2/sqrt)", "frac": achieved / peak_exp,
@@ -316,12 +320,17 @@ def main():
                                    f"(sm_max_mhz of MEASURED_PEAKS.json, {src})",
                     "kernel_ms": mm_ms,
                     "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
+        if path == 2:
+            # secondary: the implementation's own tensor-pipe work (3xTF32 distance + int8 slice
+            # products, as dense-bf16-equivalent flops) -- not the method's work
+            tf, tach, tpk = tensor_frac(cfg, world, mm_ms, pk, detail=True)
+            roofline["tensor_impl"] = {"achieved_tflops_bf16eq": tach, "peak": tpk, "frac": tf}
     launches = int(np.sum([s["gpu_launches"] for s in stats]))
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "s_per_mll_grad": ms / 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 pair kernels, f64 CG vectors",
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[path],
         "data": "synthetic (seeded; SURVEY.md §8d recipe)",
         "config": {"workload": f"{cfg.name}: exact GP MLL+grad, "
                                f"{'RBF' if cfg.kind == 0 else 'Matern-5/2'}"
@@ -334,7 +343,8 @@ def main():
         "roofline": roofline, "e2e": e2e, "gpu_launches": launches // max(len(stats), 1) * args.steps,
         "clocks": clocks,
         "detail": {k: stats[-1][k] for k in ("ms_pivchol", "ms_mbcg", "ms_matmul", "ms_slq",
-                                               "ms_deriv", "iters", "k_used", "logdet",
+                                               "ms_deriv", "ms_comm", "iters", "k_used", "logdet",
+                                               "relres_y", "relres_max", "unconverged",
                                                "matmul_path")},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

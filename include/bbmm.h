@@ -121,10 +121,10 @@ typedef struct {
                                 1 stored fp32 K (FP64ACC/FP32ACC), 2 tcgen05 exact on the
                                 fly (INT8EXACT), 3 stored K as int8 slices on tcgen05
                                 (INT8EXACT, BBMM_STORED) */
-    int32_t unconverged;     /* 1 if mBCG had not converged at exit: some column still active
-                                with tol > 0, or relres_max >= 1e-3 (SURVEY.md §8c "regime B":
-                                the Krylov iterate is then sensitive to rounding);
-                                NOT an error */
+    int32_t unconverged;     /* 1 if mBCG had not converged at exit: with tol > 0, some column
+                                still above tol after max_iter iterations; with tol == 0,
+                                relres_max >= 1e-3 (SURVEY.md §8c "regime B": the Krylov iterate
+                                is then sensitive to rounding); NOT an error */
     double relres_max;       /* max over the t + 1 columns of ||r_c|| / ||b_c|| at exit */
     double ms_comm;          /* device time inside the collectives (all-reduces, all-gathers)
                                 on the context stream, incl. waiting for peers; 0 single-rank */

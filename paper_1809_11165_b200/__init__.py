@@ -173,9 +173,16 @@ class Context:
         return self._stream
 
     def set_comm(self, group=None):
-        """Create the NCCL communicator over torch.distributed's world (or `group`)."""
+        """Create the NCCL communicator over torch.distributed's world (or `group`).  Without an
+        initialised process group: a 1-rank communicator (every collective is still issued)."""
         torch = _torch()
         import torch.distributed as dist
+        if group is None and not dist.is_initialized():
+            buf = (C.c_char * 128)()
+            self.check(_lib.bbmm_nccl_unique_id(C.cast(buf, _p)))
+            self.check(_lib.bbmm_ctx_set_comm(self._h, 1, 0, C.cast(buf, _p)))
+            self.nranks, self.rank = 1, 0
+            return self
         ws, rk = dist.get_world_size(group), dist.get_rank(group)
         buf = (C.c_char * 128)()
         if rk == 0:

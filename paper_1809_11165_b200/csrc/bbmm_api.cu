@@ -76,12 +76,8 @@ struct CommSpan {   // pool events bracketing one collective on the context stre
         try { record(); } catch (...) {}
     }
     void record() {
-        if (ctx->n_comm_ev >= ctx->comm_events.size()) {
-            cudaEvent_t e;
-            BBMM_CUDA(cudaEventCreate(&e));
-            ctx->comm_events.push_back(e);
-        }
-        BBMM_CUDA(cudaEventRecord(ctx->comm_events[ctx->n_comm_ev++], ctx->stream));
+        comm_events_reserve(ctx, ctx->n_comm_ev + 1);
+        record_event(ctx, ctx->comm_events[ctx->n_comm_ev++]);
     }
 };
 }  // namespace
@@ -360,6 +356,7 @@ bbmm_status_t bbmm_ctx_destroy(bbmm_ctx_t ctx) {
     if (ctx->pinned_flag) cudaFreeHost(ctx->pinned_flag);
     for (cudaEvent_t e : ctx->mm_events) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->comm_events) cudaEventDestroy(e);
+    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -753,7 +750,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                 s.relres_max = std::max(s.relres_max, o.relres[col]);
                 active |= tol > 0.0 && o.iters[col] >= max_iter && o.relres[col] >= tol;
             }
-            s.unconverged = (active || s.relres_max >= kUnconvergedRelres) ? 1 : 0;
+            s.unconverged = (tol > 0.0 ? active : s.relres_max >= kUnconvergedRelres) ? 1 : 0;
             s.ms_comm = comm_timing_ms(ctx);
             *stats_h = s;
         }

@@ -120,9 +120,20 @@ struct bbmm_ctx_s {
     // last comm_timing_reset, reused across calls like mm_events
     std::vector<cudaEvent_t> comm_events;
     size_t n_comm_ev = 0;
+    bool capturing = false;   // the context stream is being captured into a CUDA graph (mBCG)
+    cudaGraphExec_t graph_exec = nullptr;   // the last call's captured mBCG iterations
 };
 
 namespace bbmm {
+
+// Timing events on the context stream.  While the mBCG iterations are captured into a CUDA
+// graph the record must be an external event-record node (a plain record on a capturing stream
+// is only a dependency marker and would leave the event unrecorded).
+inline void record_event(bbmm_ctx_s *ctx, cudaEvent_t ev) {
+    cudaError_t e = ctx->capturing ? cudaEventRecordWithFlags(ev, ctx->stream, cudaEventRecordExternal)
+                                   : cudaEventRecord(ev, ctx->stream);
+    if (e != cudaSuccess) throw Error{BBMM_ERR_CUDA, std::string("event record: ") + cudaGetErrorString(e)};
+}
 
 // --------------------------------------------------------------- helpers
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -265,6 +276,7 @@ struct MbcgOut {
     int n_ev_ = 0;   // ctx->mm_events[0, n_ev_) bracket the matmuls of this run (pairs)
 };
 cudaEvent_t mm_event(bbmm_ctx_s *ctx, size_t i);
+void comm_events_reserve(bbmm_ctx_s *ctx, size_t n);
 void precond_setup(bbmm_ctx_s *ctx, const double *L, int64_t n, int k, double noise_var,
                    double *cholC, double *logdet_d);
 // sor.cu: Bs = Lu^{-1} K_UX (m x n fp64, replicated), K_SoR = Bs^T Bs

@@ -679,7 +679,7 @@ bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c) {
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                  const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
                  double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
-    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    if (ev0) record_event(ctx, ev0);
     int sp = 1;
     const int da = tc2_da(d);
     if (mode == 1) {
@@ -691,7 +691,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
             else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
             else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported derivative shape"};
         }
-        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        if (ev1) record_event(ctx, ev1);
         return sp;
     }
     if (mode == 2) {   // Matern-5/2
@@ -703,7 +703,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
             else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
             else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported Matern shape"};
         }
-        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        if (ev1) record_event(ctx, ev1);
         return sp;
     }
 #define BBMM_TC2(CC, DD) \
@@ -717,7 +717,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         throw Error{BBMM_ERR_ARG, "k1tc2: unsupported (c, d)"};
     }
 #undef BBMM_TC2
-    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    if (ev1) record_event(ctx, ev1);
     return sp;
 }
 

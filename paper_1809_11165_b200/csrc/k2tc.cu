@@ -453,7 +453,7 @@ TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const f
 int k2tc_matmul(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const double *S, int c,
                 int64_t n, int64_t nloc, double s, double *Vpart, size_t cap, cudaEvent_t ev0,
                 cudaEvent_t ev1) {
-    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    if (ev0) record_event(ctx, ev0);
     int sp = 1;
     const int64_t npad = k1tc_pad_rows(n);
     if (nloc > 0) {
@@ -470,7 +470,7 @@ int k2tc_matmul(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const dou
             default: throw Error{BBMM_ERR_ARG, "k2tc: unsupported column count"};
         }
     }
-    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    if (ev1) record_event(ctx, ev1);
     return sp;
 }
 

@@ -258,9 +258,9 @@ int kernel_matmul_onthefly(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, i
                            double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1) {
     int splits = choose_splits(n, nloc, 128, 6 * kNumSMs);
     BBMM_REQUIRE((size_t)splits * nloc * round4(cp) <= cap, "Vpart workspace too small");
-    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    if (ev0) record_event(ctx, ev0);
     if (nloc == 0) {
-        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        if (ev1) record_event(ctx, ev1);
         return splits;
     }
     if (kind == BBMM_RBF) {
@@ -272,7 +272,7 @@ int kernel_matmul_onthefly(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, i
     }
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
-    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    if (ev1) record_event(ctx, ev1);
     return splits;
 }
 
@@ -299,9 +299,9 @@ int kernel_matmul_stored(bbmm_ctx_s *ctx, const float *Kst, int64_t n, int64_t n
     BBMM_REQUIRE((size_t)splits * nloc * round4(cp) <= cap, "Vpart workspace too small");
     int64_t jchunk = ceil_div(ceil_div(n, splits), 128) * 128;
     dim3 grid((unsigned)ceil_div(nloc, 32), (unsigned)splits);
-    if (ev0) BBMM_CUDA(cudaEventRecord(ev0, ctx->stream));
+    if (ev0) record_event(ctx, ev0);
     if (nloc == 0) {
-        if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+        if (ev1) record_event(ctx, ev1);
         return splits;
     }
     if (acc64) {
@@ -311,7 +311,7 @@ int kernel_matmul_stored(bbmm_ctx_s *ctx, const float *Kst, int64_t n, int64_t n
     }
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
-    if (ev1) BBMM_CUDA(cudaEventRecord(ev1, ctx->stream));
+    if (ev1) record_event(ctx, ev1);
     return splits;
 }
 

@@ -14,6 +14,7 @@
 //   relres = |R| / |B| (freeze if < tol) ; S = C^{-1} L^T R ;
 //   Z = (R - L S)/sigma^2 ; rho' = <R,Z> ; beta = rho'/rho ; D = Z + beta D.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "bbmm_internal.cuh"
@@ -458,6 +459,24 @@ __global__ void k_after_B(MbcgState *st, const double *__restrict__ red, const d
     if (k > 0) chol_solve_warps(cholC, k, red + c, S, c);
 }
 
+// rho' = R^T Phat^{-1} R from the already reduced |R|^2 (red[0..c)) and W = L^T R (red[c..)):
+// with S = C^{-1} W and Phat^{-1} = (I - L C^{-1} L^T) / sigma^2 (Woodbury, reading R10),
+//   R^T Phat^{-1} R = (|R|^2 - W^T S) / sigma^2        (k = 0: Phat = I, rho' = |R|^2).
+// Used by multi-rank runs, where it replaces the all-reduce of the local <R, Z> partials
+// (two small all-reduces per iteration instead of three).
+__global__ void k_rz_identity(const double *__restrict__ red, const double *__restrict__ S, int k,
+                              int c, double noise_var, double *__restrict__ rz) {
+    const int col = threadIdx.x;
+    if (col >= c) return;
+    double v = red[col];
+    if (k > 0) {
+        double ws = 0.0;
+        for (int m = 0; m < k; m++) ws = fma(red[c + (int64_t)m * c + col], S[(int64_t)m * c + col], ws);
+        v = (v - ws) / noise_var;
+    }
+    rz[col] = v;
+}
+
 // S = C^{-1} W at initialisation (red = W).
 __global__ void k_solve_S(const double *__restrict__ W, const double *cholC, int k, int c,
                           double *__restrict__ S) {
@@ -706,6 +725,14 @@ void make_probes(bbmm_ctx_s *ctx, const int8_t *eps, uint64_t seed, int64_t n, i
     ctx->launches++;
 }
 
+void comm_events_reserve(bbmm_ctx_s *ctx, size_t n) {
+    while (ctx->comm_events.size() < n) {
+        cudaEvent_t e;
+        BBMM_CUDA(cudaEventCreate(&e));
+        ctx->comm_events.push_back(e);
+    }
+}
+
 cudaEvent_t mm_event(bbmm_ctx_s *ctx, size_t i) {
     while (ctx->mm_events.size() <= i) {
         cudaEvent_t e;
@@ -828,7 +855,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
                                            (int)((size_t)msor * c * 8)));
     }
     auto sor_matmul = [&](cudaEvent_t e0, cudaEvent_t e1) {
-        if (e0) BBMM_CUDA(cudaEventRecord(e0, sm));
+        if (e0) record_event(ctx, e0);
         if (nloc > 0) {
             launch_ltr(a.sor_B, msor, D, part_sor, smem_sor);
             k_reduce_blocks<<<reduce_grid(msor * c), 256, 0, sm>>>(part_sor, ltr_blocks, msor * c,
@@ -844,7 +871,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
                                                              cs, Vpart);
             launches++;
         }
-        if (e1) BBMM_CUDA(cudaEventRecord(e1, sm));
+        if (e1) record_event(ctx, e1);
         return 1;
     };
     // precondition apply: grid (row blocks, column chunks of 8); partials nblk x c
@@ -854,6 +881,14 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
                                                       c, Z, part);
         reduce(c, dst);
         launches++;
+    };
+    // multi-rank: Z only; rho' comes from k_rz_identity (no third all-reduce)
+    auto precond_apply_z = [&](double *) {
+        if (nloc > 0) {
+            k_precond_apply<<<pa_grid, 256, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R,
+                                                          nloc, c, Z, part);
+            launches++;
+        }
     };
 
     // ---------------- initialisation: R = B, Z = P^{-1} R, D = Z
@@ -868,8 +903,13 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         launches++;
     }
     double *red_rz = red + (size_t)(kk + 1) * c;
-    precond_apply(red_rz);
-    if (multi) allreduce_sum(ctx, red_rz, c);
+    if (multi) {
+        precond_apply_z(red_rz);
+        k_rz_identity<<<1, 64, 0, sm>>>(red, S, k, c, a.noise_var, red_rz);
+        launches++;
+    } else {
+        precond_apply(red_rz);
+    }
     k_init_state<<<1, 64, 0, sm>>>(st, red, red_rz, c);
     launches++;
     if (out.Z0) {
@@ -919,7 +959,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     if (a.tol > 0.0 && !ctx->pinned_flag) BBMM_CUDA(cudaMallocHost(&ctx->pinned_flag, sizeof(int)));
     int *any_h = ctx->pinned_flag;
     int iters_run = 0;
-    for (int j = 0; j < a.max_iter; j++) {
+    // one mBCG iteration (Alg. S2 body); false = stop (every column converged, tol > 0)
+    auto iterate = [&](int j) -> bool {
         cudaEvent_t e0 = mm_event(ctx, 2 * (size_t)j), e1 = mm_event(ctx, 2 * (size_t)j + 1);
         int splits;
         if (use_sor)
@@ -938,39 +979,73 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
                        use_tc ? Bp : nullptr, tc_nd, tc_rows, Stc,
                        use_tc ? k1tc_pad_rows(a.n) : 0};
             mbcg_fused_iteration(ctx, fplan, io);
-            BBMM_LAUNCH_CHECK();
-            iters_run = j + 1;
-            if (a.tol > 0.0) {
-                BBMM_CUDA(cudaMemcpyAsync(any_h, &st->any_active, sizeof(int),
-                                          cudaMemcpyDeviceToHost, sm));
-                BBMM_CUDA(cudaStreamSynchronize(sm));
-                if (!*any_h) break;
+        } else {
+            k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
+            reduce(c, red);
+            if (multi) allreduce_sum(ctx, red, c);
+            k_alpha<<<1, 64, 0, sm>>>(st, red, ahist, c);
+            k_passB<<<g.grid, g.block, 0, sm>>>(st, D, V, nloc, c, U, R, part);
+            reduce(c, red);
+            LtR(red + c);
+            if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
+            k_after_B<<<1, kSolveThreads, (size_t)(kSolveThreads / 32) * std::max(k, 1) * 8, sm>>>(
+                st, red, cholC, k, c, a.tol, S, rhist);
+            if (multi) {
+                precond_apply_z(red_rz);
+                k_rz_identity<<<1, 64, 0, sm>>>(red, S, k, c, a.noise_var, red_rz);
+                launches++;
+            } else {
+                precond_apply(red_rz);
             }
-            continue;
+            k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
+            launches += 7;
+            passD(1);
         }
-        k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
-        reduce(c, red);
-        if (multi) allreduce_sum(ctx, red, c);
-        k_alpha<<<1, 64, 0, sm>>>(st, red, ahist, c);
-        k_passB<<<g.grid, g.block, 0, sm>>>(st, D, V, nloc, c, U, R, part);
-        reduce(c, red);
-        LtR(red + c);
-        if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
-        k_after_B<<<1, kSolveThreads, (size_t)(kSolveThreads / 32) * std::max(k, 1) * 8, sm>>>(
-            st, red, cholC, k, c, a.tol, S, rhist);
-        precond_apply(red_rz);
-        if (multi) allreduce_sum(ctx, red_rz, c);
-        k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
-        launches += 7;
-        passD(1);
         BBMM_LAUNCH_CHECK();
         iters_run = j + 1;
         if (a.tol > 0.0) {
             BBMM_CUDA(cudaMemcpyAsync(any_h, &st->any_active, sizeof(int), cudaMemcpyDeviceToHost,
                                       sm));
             BBMM_CUDA(cudaStreamSynchronize(sm));
-            if (!*any_h) break;
+            if (!*any_h) return false;
         }
+        return true;
+    };
+    // With tol == 0 the iteration count is fixed, so the per-step path (large n, multi-rank over
+    // NCCL) captures iterations 1..p-1 -- kernels, collectives and the timing events -- into ONE
+    // CUDA graph and launches it once: no per-kernel launch gaps between the ~12 kernels and
+    // 4 collectives of an iteration.  Iteration 0 runs eagerly (first-use workspace and kernel
+    // attributes are set up outside the capture).  The in-process rank group is host-staged and
+    // cannot be captured; BBMM_NO_GRAPH=1 turns the capture off (A/B tests).
+    const bool graph = !fused && a.tol == 0.0 && !ctx->local && a.max_iter >= 2 &&
+                       !std::getenv("BBMM_NO_GRAPH");
+    if (ctx->graph_exec) {            // the previous call's graph (that call has synchronised)
+        cudaGraphExecDestroy(ctx->graph_exec);
+        ctx->graph_exec = nullptr;
+    }
+    if (graph) {
+        iterate(0);
+        mm_event(ctx, 2 * (size_t)a.max_iter - 1);            // create the events outside the capture
+        comm_events_reserve(ctx, ctx->n_comm_ev + 8 * (size_t)a.max_iter + 8);
+        BBMM_CUDA(cudaStreamBeginCapture(sm, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        cudaGraph_t gr = nullptr;
+        try {
+            for (int j = 1; j < a.max_iter; j++) iterate(j);
+        } catch (...) {
+            ctx->capturing = false;
+            if (cudaStreamEndCapture(sm, &gr) == cudaSuccess && gr) cudaGraphDestroy(gr);
+            throw;
+        }
+        ctx->capturing = false;
+        BBMM_CUDA(cudaStreamEndCapture(sm, &gr));
+        const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, gr, 0);
+        cudaGraphDestroy(gr);
+        BBMM_CUDA(ie);
+        BBMM_CUDA(cudaGraphLaunch(ctx->graph_exec, sm));
+    } else {
+        for (int j = 0; j < a.max_iter; j++)
+            if (!iterate(j)) break;
     }
     // ---------------- outputs
     if (out.U) {

@@ -199,3 +199,62 @@ def test_train_adam_partitioned_matches_single_rank(orc):
     np.testing.assert_array_equal(parts[0][0], parts[1][0])
     np.testing.assert_allclose(parts[0][0], th1, rtol=0, atol=1e-8)
     np.testing.assert_allclose(parts[0][1][:, 0], tr1[:, 0], rtol=1e-8)
+
+
+@pytest.mark.parametrize("name,n,kmode", [("C4", 3000, bb.ONTHEFLY), ("C1", 3338, bb.STORED),
+                                          ("C3", 2000, bb.ONTHEFLY)])
+def test_nccl_single_rank_communicator(orc, name, n, kmode):
+    """The NCCL transport on real hardware: a 1-rank NCCL communicator (bbmm_ctx_set_comm with
+    nranks = 1) makes the library issue every collective of the multi-GPU path -- all-reduces
+    of the dots, the column-max all-reduce, the all-gathers of the packed search directions and
+    of the derivative operands -- through NCCL, inside the captured CUDA graph of the mBCG
+    iterations, with rho' from the Woodbury identity.  Results match the communicator-free call
+    (per-step kernels) and the oracle; the stats attribute time to the collectives."""
+    import os
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=0)
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        return bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=7, kmode=kmode,
+                               return_solves=True)
+
+    one = single(call)
+    ctx = bb.Context(0).set_comm()
+    try:
+        g = call(ctx)
+        g2 = call(ctx)                                   # the context is reusable
+    finally:
+        ctx.close()
+    assert g["stats"]["ms_comm"] > 0.0
+    assert g2["mll"] == g["mll"]
+    assert colwise_rel(g["U"].cpu().numpy(), one["U"].cpu().numpy()).max() < 1e-8
+    assert abs(g["mll"] - one["mll"]) <= 1e-10 * abs(one["mll"])
+    assert np.linalg.norm(g["grad"] - one["grad"]) <= 1e-8 * np.linalg.norm(one["grad"])
+    o = orc.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, cfg.t, cfg.k,
+                         cfg.p, seed=7)
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+
+
+def test_graph_capture_matches_eager_iterations(orc):
+    """The captured mBCG iterations (tol = 0, per-step kernels) against the same iterations
+    launched one by one (BBMM_NO_GRAPH=1): bit-identical results."""
+    import os
+    cfg = synth.scaled(synth.CONFIGS["C4"], 3000)
+    pr = synth.make_problem(cfg, seed=0)
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        return bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=7, return_solves=True)
+
+    a = single(call)
+    os.environ["BBMM_NO_GRAPH"] = "1"
+    try:
+        b = single(call)
+    finally:
+        os.environ.pop("BBMM_NO_GRAPH", None)
+    assert a["mll"] == b["mll"]
+    np.testing.assert_array_equal(a["grad"], b["grad"])
+    np.testing.assert_array_equal(a["U"].cpu().numpy(), b["U"].cpu().numpy())
+    assert a["stats"]["ms_matmul"] > 0 and a["stats"]["matmul_launches"] == cfg.p

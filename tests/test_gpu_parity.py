@@ -433,3 +433,76 @@ def test_matern_tc_matmul_matches_oracle(ctx, orc, n, c):
     err = np.abs(V - ref)
     bound = matmul_bound(orc, pr, D)
     assert np.all(err <= bound), float((err / bound).max())
+
+
+# ------------------------------------------------- tol > 0 and breakdown (R9, R24)
+@pytest.mark.parametrize("name,n,fused,tol", [("C1", 3338, True, 1e-3), ("C4", 3000, True, 1e-3),
+                                              ("C4", 3000, False, 1e-3), ("C2", 2500, False, 1e-2)])
+def test_mll_and_grad_with_tolerance_matches_oracle(ctx, orc, name, n, fused, tol, monkeypatch):
+    """tol > 0 (reading R9, PAPER.md:333 Alg. S2): columns freeze once ||r_c||/||b_c|| < tol, the
+    tridiagonals are truncated at each column's iteration count, the loop exits early once every
+    column has converged.  Same tol on both sides; both the fused single-kernel iteration and the
+    per-step kernels."""
+    if not fused:
+        monkeypatch.setenv("BBMM_NO_FUSED_MBCG", "1")
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    if name == "C4":        # rank 100 converges in one iteration at n = 3000; rank 10 takes 7
+        cfg = synth.dataclasses.replace(cfg, k=10)
+    pr = synth.make_problem(cfg, seed=0)
+    km = bb.STORED if cfg.stored else bb.ONTHEFLY
+    g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), cfg.t, cfg.k, cfg.p, tol=tol,
+                        seed=7, kmode=km, return_solves=True)
+    o = orc.mll_and_grad(cfg.kind, pr.X, pr.y, pr.log_ls, pr.log_s, pr.log_noise, cfg.t, cfg.k,
+                         cfg.p, tol=tol, seed=7)
+    st = g["stats"]
+    assert st["iters"] == int(o["iters"]) and st["iters"] < cfg.p, (st["iters"], o["iters"])
+    assert st["unconverged"] == 0 and st["relres_max"] < tol
+    assert abs(st["logdet"] - o["logdet"]) <= 1e-3 * abs(o["logdet"])
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
+    # solves of a frozen column agree up to the stopping tolerance's own slack
+    assert colwise_rel(g["U"].cpu().numpy(), o["U"]).max() < 1e-4
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_breakdown_is_numeric_error_and_context_survives(ctx, orc, fused, monkeypatch):
+    """An operator that is not positive definite in floating point -- every point identical, so
+    K = s 11^T (rank one), and sigma^2 underflowed to 0 -- breaks mBCG down (alpha <= 0 or
+    non-finite, reading R24): BBMM_ERR_NUMERIC (4) on the GPU, ORC_ERR_NUMERIC on the oracle, and
+    the context keeps working afterwards."""
+    if not fused:
+        monkeypatch.setenv("BBMM_NO_FUSED_MBCG", "1")
+    n, t = 64, 4
+    X = np.zeros((n, 2), np.float32)
+    y = synth.random_block(n, 1, seed=3)[:, 0].copy()
+    h = bb.Hyper(bb.RBF, np.array([0.0]), 0.0, -1000.0)
+    with pytest.raises(bb.BBMMError) as e:
+        bb.mll_and_grad(ctx, dev(X), dev(y), h, t, 0, 10, seed=7)
+    assert e.value.status == 4, e.value
+    with pytest.raises(orc.OracleError):
+        orc.mll_and_grad(bb.RBF, X, y, [0.0], 0.0, -1000.0, t, 0, 10, seed=7)
+    cfg = synth.scaled(synth.CONFIGS["C0"], 256)
+    pr, g, o = run_both(ctx, orc, cfg)
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+
+
+def test_binding_rejects_wrong_sizes(ctx):
+    """The C-ABI receives raw pointers, so the binding checks every size it passes:
+    a wrong-sized y, D, B, L or eps raises ValueError before any launch."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 300)
+    pr = synth.make_problem(cfg, seed=0)
+    X, h = dev(pr.X), hyper_of(pr)
+    with pytest.raises(ValueError):
+        bb.mll_and_grad(ctx, X, dev(pr.y[:-1]), h, 3, 5)
+    with pytest.raises(ValueError):
+        bb.kernel_matmul(ctx, X, dev(np.zeros((299, 3)), torch.float64), h)
+    with pytest.raises(ValueError):
+        bb.mbcg(ctx, X, h, dev(np.zeros((301, 3)), torch.float64))
+    with pytest.raises(ValueError):
+        bb.mbcg(ctx, X, h, dev(np.zeros((300, 3)), torch.float64), L=dev(np.zeros((5, 299)), torch.float64))
+    with pytest.raises(ValueError):
+        bb.mll_and_grad(ctx, X, dev(pr.y), h, 3, 5, eps=dev(np.ones((300, 3)), torch.int8))
+    with pytest.raises(ValueError):
+        bb.kernel_matmul(ctx, X[:, :1].reshape(-1), dev(np.zeros((300, 3)), torch.float64), h)
+    g = bb.mll_and_grad(ctx, X, dev(pr.y), h, 3, 5)          # still fine afterwards
+    assert np.isfinite(g["mll"])
