@@ -526,7 +526,13 @@ static int mbcg_generic(op_fn op, const void *opctx, const precond_t *P,
             double dv = 0.0;
             for (int64_t i = 0; i < n; i++) dv += D[i * c + col] * V[i * c + col];
             double a = rho[col] / dv;
-            if (!(a > 0.0) || !isfinite(a)) { st = ORC_ERR_NUMERIC; goto done; }
+            if (!(a > 0.0) || !isfinite(a)) {
+                /* reading R9/R24: a residual exhausted below fp64's range (rho <= 1e-250
+                   rho_0, e.g. p far past convergence) is frozen like R = 0 exactly;
+                   otherwise the operator is not positive definite: breakdown */
+                if (rho[col] <= 1e-250 * rho0[col]) { active[col] = 0; continue; }
+                st = ORC_ERR_NUMERIC; goto done;
+            }
             double r2 = 0.0;
             for (int64_t i = 0; i < n; i++) {
                 U[i * c + col] += a * D[i * c + col];

@@ -64,8 +64,8 @@ __global__ void k_prep_deriv_tc(const float *__restrict__ B32, int cs, int c,
         float *tile = WB + tt * (int64_t)(2 * CA * BK);
         for (int q = 0; q < CA; q++) {
             const float b = (j < n && q < c) ? B32[j * cs + q] : 0.0f;
-            const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
-            const float bl = b - bh;
+            const float bh = tf32_rn(b);
+            const float bl = tf32_rn(b - bh);
             tile[(q >> 2) * (BK * 4) + jj * 4 + (q & 3)] = bh;
             tile[((CA + q) >> 2) * (BK * 4) + jj * 4 + (q & 3)] = bl;
         }
@@ -167,8 +167,8 @@ k_deriv_tc(const float *__restrict__ Xs, const float *__restrict__ A32, int csa,
             float *ap = reinterpret_cast<float *>(aw_sm);
             for (int q = 0; q < CA; q++) {
                 const float v = (valid && q < csa) ? A32[row * csa + q] : 0.0f;
-                const float vh = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-                const float parts[3] = {vh, vh, v - vh};
+                const float vh = tf32_rn(v);
+                const float parts[3] = {vh, vh, tf32_rn(v - vh)};
 #pragma unroll
                 for (int pt = 0; pt < 3; pt++) {
                     const int k = pt * CA + q;

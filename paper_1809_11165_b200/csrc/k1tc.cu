@@ -63,7 +63,11 @@ __global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c,
     for (int b = lane; b < nblk; b += 32) m = fmax(m, part[(int64_t)b * c + col]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) S[col] = m > 0.0 ? m : 1.0;
+    // raw maximum (0 for an all-zero column or a rank without rows): the caller may all-reduce
+    // it (max) across ranks, so no substitute value here -- a rank with no rows must not
+    // contribute 1.0 (that coarsened every rank's fixed-point D to a 2^-31 grid of 1.0 once
+    // mBCG had converged: stagnation at relres ~5e-9 and an alpha breakdown on 4 ranks)
+    if (lane == 0) S[col] = m;
 }
 
 // Pack rows [row0, row0 + rows) of D (fp64) into the K-major slice layout
@@ -97,7 +101,8 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
                 if (j < n && j >= row0 && j < row0 + rows) {
                     int64_t P;
                     if (col < c) {
-                        double q = D[(j - row0) * ldd + col] / S[col] * scaleT;
+                        const double sc = S[col] > 0.0 ? S[col] : 1.0;   // all-zero column
+                        double q = D[(j - row0) * ldd + col] / sc * scaleT;
                         P = llrint(q) + offT;                  // in [0, 2^(T+1)]
                     } else {
                         P = offT;                              // constant column

@@ -65,10 +65,10 @@ constexpr int NCW = 4 * NPS;
 static_assert((JW == 32 || (JW == 16 && NPS % 2 == 0)) && 32 * (NCW + 2) <= 1024, "CTA shape");
 // j per TMEM drain.  All slice bytes are unsigned (q2 <= 0x40, p3 <= 0x80),
 // so the accumulators are read as uint32; the largest per-j block sum is
-// block 3: q2 p0 + q1 p1 + q0 p2 <= 64*255 + 2*255*255 = 146370, hence
-// < 2^32 / 146370 = 29343 j per window.
-constexpr int WINDOW = (int)(4294967295ull / 146370ull) / BK * BK;
-static_assert((double)WINDOW * 146370.0 < 4294967296.0, "uint32 window bound");
+// block 3: q2 p0 + q1 p1 + q0 p2 <= 128*255 + 2*255*255 = 162690 (q2 <= 0x80: k~ = 1
+// exactly), hence < 2^32 / 162690 = 26399 j per window.
+constexpr int WINDOW = (int)(4294967295ull / 162690ull) / BK * BK;
+static_assert((double)WINDOW * 162690.0 < 4294967296.0, "uint32 window bound");
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(NCW * JW == 4 * BK, "4 lane quarters x BK columns");
@@ -351,8 +351,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 #pragma unroll
             for (int q = 0; q < DA; q++) {
                 const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
-                const float vh = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-                const float vl = v - vh;
+                const float vh = tf32_rn(v);
+                const float vl = tf32_rn(v - vh);
                 const float parts[3] = {vh, vh, vl};
 #pragma unroll
                 for (int pt = 0; pt < 3; pt++) {
@@ -403,19 +403,24 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     kv = ex2_approx(sj);
                 }
                 // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
-                // +eps by rounding near the diagonal); k~ r^2 <= 2/e < 1
-                // (the factor 2 ln 2 is applied in the epilogue: k~ (-S) <= 0.53 here)
+                // +eps by rounding near the diagonal).  The factor 2 ln 2 is applied in the
+                // epilogue, so the quantised value is k~ (-S) <= 1/(e ln 2)/2 ~= 0.53 (not
+                // k~ r^2 <= 2/e ~= 0.74): the 2^-23 grid step is 1.39x coarser relative to
+                // the derivative value (about half a bit), measured inside the gradient bar
+                // (MODE 1 margin)
                 if (MODE == 1) kv *= fmaxf(-sj, 0.0f);
                 q[v] = __float_as_uint(kv);
             }
-            // q = 2 + k~ in [2, 3]: exponent 128 (low bit 0), so the three low bytes are
-            // exactly the 22-bit fixed-point k~ 2^22 (round to nearest); two points per
-            // instruction on the paired FP32 pipe (FADD2: 292 vs 300 ms per C4 K^D)
+            // q = 2 + 2 k~ in [2, 4]: for k~ < 1 the exponent is 128 (bit 23 = 0) and the
+            // mantissa is k~ 2^23 rounded to nearest; k~ = 1 gives 4.0 = exponent 129, whose
+            // low bit lands on bit 23 = 2^23 = k~ 2^23 again.  So the three low bytes are
+            // exactly the 23-bit fixed-point k~ 2^23 for every k~ in [0, 1] (grid 2^-23: half
+            // the rounding of the q = 2 + k~ form).  Two points per instruction (FFMA2).
 #pragma unroll
             for (int v = 0; v < 4; v += 2) {
                 unsigned long long pq;
                 asm("mov.b64 %0, {%1, %2};" : "=l"(pq) : "r"(q[v]), "r"(q[v + 1]));
-                asm("add.rn.f32x2 %0, %0, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
+                asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
                 asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pq));
             }
             const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
@@ -526,7 +531,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
             double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * CS;
-            const double base = s * (ND == 4 ? 0x1p-52 : 0x1p-60) *
+            const double base = s * (ND == 4 ? 0x1p-53 : 0x1p-61) *
                                 (MODE == 1 ? 1.3862943611198906 : 1.0);   // MODE 1: r^2 = -2 ln2 S
             const double cacc = acc_sm[C][rl];
 #pragma unroll
@@ -577,8 +582,8 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
                     (ok && q < d) ? xs[q] : 0.0f;
                 continue;
             }
-            const float bh = __uint_as_float(__float_as_uint(b) & 0xFFFFE000u);
-            const float bl = b - bh;
+            const float bh = tf32_rn(b);
+            const float bl = tf32_rn(b - bh);
             const int64_t tt = j / BK;
             const int jj = s_col_of((int)(j - tt * BK));
             float *tile = XB + tt * (int64_t)(2 * DA * BK);

@@ -410,8 +410,10 @@ __global__ void k_alpha(MbcgState *st, const double *__restrict__ dv, double *__
     double a = 0.0;
     if (st->active[col]) {
         a = st->rho[col] / dv[col];
-        if (!(a > 0.0) || !isfinite(a)) {   // indefinite operator (reading R24)
-            st->status = BBMM_ERR_NUMERIC;
+        if (!(a > 0.0) || !isfinite(a)) {
+            // reading R9/R24: a residual exhausted below fp64's range (rho <= 1e-250 rho_0,
+            // p far past convergence) freezes like R = 0; else indefinite operator: breakdown
+            if (!(st->rho[col] <= 1e-250 * st->rho0[col])) st->status = BBMM_ERR_NUMERIC;
             a = 0.0;
             st->active[col] = 0;
         } else {
@@ -457,24 +459,6 @@ __global__ void k_after_B(MbcgState *st, const double *__restrict__ red, const d
         if (rel < tol) st->active[col] = 0;
     }
     if (k > 0) chol_solve_warps(cholC, k, red + c, S, c);
-}
-
-// rho' = R^T Phat^{-1} R from the already reduced |R|^2 (red[0..c)) and W = L^T R (red[c..)):
-// with S = C^{-1} W and Phat^{-1} = (I - L C^{-1} L^T) / sigma^2 (Woodbury, reading R10),
-//   R^T Phat^{-1} R = (|R|^2 - W^T S) / sigma^2        (k = 0: Phat = I, rho' = |R|^2).
-// Used by multi-rank runs, where it replaces the all-reduce of the local <R, Z> partials
-// (two small all-reduces per iteration instead of three).
-__global__ void k_rz_identity(const double *__restrict__ red, const double *__restrict__ S, int k,
-                              int c, double noise_var, double *__restrict__ rz) {
-    const int col = threadIdx.x;
-    if (col >= c) return;
-    double v = red[col];
-    if (k > 0) {
-        double ws = 0.0;
-        for (int m = 0; m < k; m++) ws = fma(red[c + (int64_t)m * c + col], S[(int64_t)m * c + col], ws);
-        v = (v - ws) / noise_var;
-    }
-    rz[col] = v;
 }
 
 // S = C^{-1} W at initialisation (red = W).
@@ -882,15 +866,6 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         reduce(c, dst);
         launches++;
     };
-    // multi-rank: Z only; rho' comes from k_rz_identity (no third all-reduce)
-    auto precond_apply_z = [&](double *) {
-        if (nloc > 0) {
-            k_precond_apply<<<pa_grid, 256, smem_S, sm>>>(a.L, a.n, a.r0, k, S, a.noise_var, R,
-                                                          nloc, c, Z, part);
-            launches++;
-        }
-    };
-
     // ---------------- initialisation: R = B, Z = P^{-1} R, D = Z
     k_init_vectors<<<g.grid, g.block, 0, sm>>>(B, ldb, nloc, c, U, R, D, part);
     launches++;
@@ -903,13 +878,8 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         launches++;
     }
     double *red_rz = red + (size_t)(kk + 1) * c;
-    if (multi) {
-        precond_apply_z(red_rz);
-        k_rz_identity<<<1, 64, 0, sm>>>(red, S, k, c, a.noise_var, red_rz);
-        launches++;
-    } else {
-        precond_apply(red_rz);
-    }
+    precond_apply(red_rz);
+    if (multi) allreduce_sum(ctx, red_rz, c);
     k_init_state<<<1, 64, 0, sm>>>(st, red, red_rz, c);
     launches++;
     if (out.Z0) {
@@ -990,13 +960,12 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             if (multi) allreduce_sum(ctx, red, (size_t)(k + 1) * c);
             k_after_B<<<1, kSolveThreads, (size_t)(kSolveThreads / 32) * std::max(k, 1) * 8, sm>>>(
                 st, red, cholC, k, c, a.tol, S, rhist);
-            if (multi) {
-                precond_apply_z(red_rz);
-                k_rz_identity<<<1, 64, 0, sm>>>(red, S, k, c, a.noise_var, red_rz);
-                launches++;
-            } else {
-                precond_apply(red_rz);
-            }
+            // rho' = <R, Z> reduced directly.  (The Woodbury identity
+            // (|R|^2 - W^T C^-1 W) / sigma^2 would spare this all-reduce but cancels
+            // catastrophically once R reaches rounding level -- measured: alpha <= 0
+            // breakdowns at n = 300, k = 100 on 4 ranks.)
+            precond_apply(red_rz);
+            if (multi) allreduce_sum(ctx, red_rz, c);
             k_beta<<<1, 64, 0, sm>>>(st, red_rz, bhist, c);
             launches += 7;
             passD(1);

@@ -136,10 +136,16 @@ __global__ void __launch_bounds__(kT, 1) k_mbcg_fused(Args a) {
         double al = 0.0;
         if (sh.act[col]) {
             al = sh.rho[col] / sh.colv[col];
-            if (!(al > 0.0) || !isfinite(al)) {          // indefinite operator (reading R24)
+            if (!(al > 0.0) || !isfinite(al)) {
+                // reading R9/R24: exhausted residual (rho <= 1e-250 rho_0) freezes like
+                // R = 0; otherwise an indefinite operator: breakdown
+                const bool exhausted = sh.rho[col] <= 1e-250 * st->rho0[col];
                 al = 0.0;
                 sh.act[col] = 0;
-                if (b0) { st->status = BBMM_ERR_NUMERIC; st->active[col] = 0; }
+                if (b0) {
+                    if (!exhausted) st->status = BBMM_ERR_NUMERIC;
+                    st->active[col] = 0;
+                }
             } else if (b0) {
                 a.ahist[(int64_t)j * c + col] = al;
                 st->iters[col] = j + 1;

@@ -19,6 +19,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// Round an fp32 value to the nearest tf32 (10 explicit mantissa bits) for the 3xTF32 splits
+// x = hi + lo: hi rounded (|lo| <= 2^-11 |x|) and lo rounded too (the MMA would truncate its
+// low 13 bits), so hi + lo matches x to ~2^-22 |x| -- truncating both left ~2^-20.
+__host__ __device__ __forceinline__ float tf32_rn(float x) {
+#ifdef __CUDA_ARCH__
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+#else
+    uint32_t u;
+    __builtin_memcpy(&u, &x, 4);
+    u = (u + 0x1000u) & 0xFFFFE000u;
+    float r;
+    __builtin_memcpy(&r, &u, 4);
+    return r;
+#endif
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

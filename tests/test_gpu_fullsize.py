@@ -45,8 +45,8 @@ REGIME_B_GRAD = 5e-3
 
 def _regime_b_solve_bar(name, n):
     path = os.path.join(LARGE, f"{name}_n{n}_floor.json")
-    if not os.path.exists(path):
-        pytest.skip(f"{path} missing (scripts/oracle_rounding_floor.py {name}:{n})")
+    if not os.path.exists(path):       # no measured floor: the strict bar
+        return 1e-4
     return max(1e-4, 2.0 * json.load(open(path))["solve_floor_max"])
 
 
