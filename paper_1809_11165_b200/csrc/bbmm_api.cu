@@ -454,14 +454,14 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
             double *S = (double *)ctx->ws.get("tc_S", kMaxCols * 8);
             k1tc_colmax(ctx, D, ldd, n, ncols, S);
             const int nd = tc_dslices(op);
-            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * tc_bslice_rows(ncols, nd));
-            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp, nd);
-            size_t cap = tc_vpart_elems(op, n, nloc, ncols);
+            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * tc_bslice_rows(op.cb, nd));
+            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp, nd, op.cb);
+            size_t cap = tc_vpart_elems(op, n, nloc, op.cb);
             double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
-            int splits = tc_matmul(ctx, op, Bp, S, ncols, n, rr.r0, nloc, h.s, Vpart, cap, nullptr,
+            int splits = tc_matmul(ctx, op, Bp, S, op.cb, n, rr.r0, nloc, h.s, Vpart, cap, nullptr,
                                    nullptr);
             k_matmul_finish<<<grid_for(nloc * ncols), 256, 0, ctx->stream>>>(
-                Vpart, splits, (ncols + 3) & ~3, nloc, ncols, h.noise_var, D, ldd, rr.r0, V, ldv);
+                Vpart, splits, tc_vstride(op), nloc, ncols, h.noise_var, D, ldd, rr.r0, V, ldv);
             BBMM_LAUNCH_CHECK();
             ctx->launches++;
             BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -627,23 +627,24 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             double *Bd = (double *)ws.get("d_Bd", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
             double *Sd = (double *)ws.get("d_S", kMaxCols * 8);
             const int64_t npad_tc = k1tc_pad_rows(rr.nb * ctx->nranks);
-            uint8_t *Bp = (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(c));
+            const int cbd = k1tc2_deriv_cols(d, c);          // MODE-1 instantiation (>= c)
+            uint8_t *Bp = (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(cbd));
             if (nloc > 0) {
                 k_build_bd<<<grid_for(nloc * c), 256, 0, sm>>>(o.U_d, Z0, nloc, t, Bd);
                 ctx->launches++;
             }
             k1tc_colmax(ctx, Bd, c, nloc, c, Sd);
             allreduce_max(ctx, Sd, c);
-            if (nloc > 0) k1tc_pack(ctx, Bd, c, rr.r0, nloc, n, c, Sd, Bp);
-            allgather_rows(ctx, Bp, (size_t)rr.nb * k1tc_bslice_rows(c));
-            const size_t cap = tc_vpart_elems(tcop, n, nloc, c);
+            if (nloc > 0) k1tc_pack(ctx, Bd, c, rr.r0, nloc, n, c, Sd, Bp, 4, cbd);
+            allgather_rows(ctx, Bp, (size_t)rr.nb * k1tc_bslice_rows(cbd));
+            const size_t cap = tc_vpart_elems(tcop, n, nloc, cbd);
             double *Vp = (double *)ws.get("d_Vpart", std::max<size_t>(cap, 1) * 8);
             double *dpart = (double *)ws.get("d_part", (size_t)sblk * 8);
             if (nloc > 0) {
                 // S_l at dred[0]: the k~ r^2 kernel-matmul (mode 1)
-                const int sp = tc_matmul(ctx, tcop, Bp, Sd, c, n, rr.r0, nloc, h.s, Vp, cap,
+                const int sp = tc_matmul(ctx, tcop, Bp, Sd, cbd, n, rr.r0, nloc, h.s, Vp, cap,
                                          nullptr, nullptr, 1);
-                k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, (c + 3) & ~3, nloc, t, o.U_d, dpart);
+                k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, (cbd + 3) & ~3, nloc, t, o.U_d, dpart);
                 reduce_blocks(ctx, dpart, sblk, 1, dred);
                 // S_s at dred[dp]: from the solves' residual identity (no matmul)
                 k_outputscale_term<<<sblk, 256, 0, sm>>>(o.U_d, o.R_d, B, Z0, h.noise_var, nloc,

@@ -188,10 +188,14 @@ int k1tc_bslice_rows(int c);
 void k1tc_col_mean(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, double *mean);
 void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, int c, double *S);
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
-               int64_t n, int c, const double *S, uint8_t *Bpack, int nd = 4);
+               int64_t n, int c, const double *S, uint8_t *Bpack, int nd = 4, int cb = -1);
 int tc_bslice_rows(int c, int nd);   // bytes per point of the packed D operand (nd slices)
 void allreduce_max(bbmm_ctx_s *ctx, double *buf, size_t count);
 bool k1tc2_supported(int kind, int d, int c);
+// the K1-TC instantiation (column count, >= c) that runs c columns, 0 if none; the
+// derivative (MODE 1) instantiation for c (isotropic RBF), 0 if none
+int k1tc2_cols(int kind, int d, int c);
+int k1tc2_deriv_cols(int d, int c);
 int64_t k1tc2_xa_floats(int64_t npad, int d);
 int64_t k1tc2_xb_floats(int64_t npad, int d);
 float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const Hyper &h,
@@ -211,18 +215,24 @@ struct TcOperand {
     const uint8_t *Kq = nullptr;  // v3 stored K slices (this rank's rows)
     int kind = 0;               // kernel family of the operand
     int nd = 4;                 // D slices of the packed operand (k1tc_pack nd)
+    int cb = 0;                 // columns of the kernel instantiation (>= c; zero-padded)
 };
+// Vpart row stride of a tensor-core operand's matmul (the instantiation's round4(cb))
+inline int tc_vstride(const TcOperand &op) { return (op.cb + 3) & ~3; }
 int tc_dslices(const TcOperand &op);   // D slices of the operand's packed format (4 or 5)
 // Prepare the tensor-core inputs for (kind, d, c) if the INT8EXACT mode applies.
 TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, const Hyper &h,
                      int64_t npad_rows);
 size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c);
-int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
+// cb: the column count of the instantiation to run (op.cb for the mBCG operand; the
+// derivative block for mode 1); Bp packed for cb, Vpart rows of round4(cb)
+int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int cb,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
               cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0);
 
 // stored K on the int8 tensor cores (k2tc.cu)
 bool k2tc_supported(int c);
+int k2tc_cols(int c);   // instantiated column count >= c, 0 if none
 size_t k2tc_vpart_elems(int64_t n, int64_t nloc, int c);
 size_t k2tc_kq_bytes(int64_t n, int64_t nloc);
 void k2tc_build(bbmm_ctx_s *ctx, const float *X, int d, const Hyper &h, int64_t n, int64_t r0,
@@ -312,6 +322,7 @@ struct FusedIo {
     int nd, nb_rows;
     double *Stc;
     int64_t pad_end;
+    int cb;        // columns of the tensor-core instantiation (constant column at cb)
 };
 bool mbcg_fused_applicable(const bbmm_ctx_s *ctx, int c, int k, bool use_sor, int64_t nloc);
 FusedPlan mbcg_fused_plan(bbmm_ctx_s *ctx, int64_t nloc, int c, int k, const double *cholC,

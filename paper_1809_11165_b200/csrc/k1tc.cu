@@ -74,10 +74,12 @@ __global__ void k_colmax_final(const double *__restrict__ part, int nblk, int c,
 // [16-point chunk][NB rows][16 bytes] (linear in the chunk index, so any
 // multiple-of-16 j-tile is contiguous): row n = b_idx * BLK + col, b_idx
 // 0..ND-1 = bytes ND-1..0 of P' = round(D/S 2^T) + 2^T with T = 8 ND - 2
-// (ND = 4: 31-bit, K1-TC; ND = 5: 39-bit, K2-TC), col == c is the constant
-// 2^T, col > c zero padding.  One thread writes the 16 bytes of one (chunk, n).
+// (ND = 4: 31-bit, K1-TC; ND = 5 / 7: Matern / stored K).  The operand is laid out for a
+// kernel instantiated for cb >= c columns: columns c..cb-1 are zero D (P' = 2^T), column cb
+// is the constant 2^T that removes the offset, columns > cb zero padding.  One thread writes
+// the 16 bytes of one (chunk, n).
 __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_t row0,
-                               int64_t rows, int64_t n, int c, int BLK, int NB, int ND,
+                               int64_t rows, int64_t n, int c, int cb, int BLK, int NB, int ND,
                                const double *__restrict__ S, uint8_t *__restrict__ Bpack,
                                int64_t tile0, int64_t tiles) {
     const int T = 8 * ND - 2;
@@ -92,7 +94,7 @@ __global__ void k_pack_bslices(const double *__restrict__ D, int64_t ldd, int64_
         const int64_t tt = tile0 + rest / (BK / 16);
         const int bi = nn / BLK, col = nn - bi * BLK;
         uint32_t wv[4] = {0, 0, 0, 0};
-        if (bi < ND && col <= c) {
+        if (bi < ND && col <= cb) {
             const int shift = 8 * (ND - 1 - bi);
 #pragma unroll
             for (int p = 0; p < 16; p++) {
@@ -142,6 +144,8 @@ int64_t k1tc_pad_rows(int64_t n) { return ceil_div(n, 384) * 384; }
 // S (c doubles, device): column max |D| over the rows given (local rows);
 // caller all-reduces (max) across ranks if needed.
 void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, int c, double *S) {
+    // columns c.. of S (padding columns of a wider kernel instantiation) read as 0
+    if (c < kMaxCols) BBMM_CUDA(cudaMemsetAsync(S + c, 0, (size_t)(kMaxCols - c) * 8, ctx->stream));
     const int cw = c <= 32 ? 32 : 64, rb = 256 / cw;
     int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, rb), 2 * kNumSMs));
     double *part = (double *)ctx->ws.get("tc_cmax", (size_t)nblk * c * 8);
@@ -153,8 +157,9 @@ void k1tc_colmax(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t rows, in
 
 // Pack local rows [row0, row0 + rows) into Bpack (tiles covering them).
 void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int64_t rows,
-               int64_t n, int c, const double *S, uint8_t *Bpack, int nd) {
-    const int NB = tc_bslice_rows(c, nd), BLK = NB / nd;
+               int64_t n, int c, const double *S, uint8_t *Bpack, int nd, int cb) {
+    if (cb < c) cb = c;
+    const int NB = tc_bslice_rows(cb, nd), BLK = NB / nd;
     // the rank holding the last rows also writes the zero padding up to
     // k1tc_pad_rows(n) (the j-tiles read past n); the layout is linear in
     // 16-point chunks, [chunk][NB][16 B], so any tile width reads it
@@ -163,7 +168,7 @@ void k1tc_pack(bbmm_ctx_s *ctx, const double *D, int64_t ldd, int64_t row0, int6
     const int64_t tiles = ceil_div(end, tc::BK) - tile0;
     const int64_t total = tiles * (tc::BK / 16) * NB;
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 8 * kNumSMs));
-    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, BLK, NB, nd, S,
+    tc::k_pack_bslices<<<grid, 256, 0, ctx->stream>>>(D, ldd, row0, rows, n, c, cb, BLK, NB, nd, S,
                                                       Bpack, tile0, tiles);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;

@@ -603,15 +603,24 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
 // ======================================================================
 static int tc2_da(int d) { return ((d + 2 + 7) / 8) * 8; }
 
-bool k1tc2_supported(int kind, int d, int c) {
+// The instantiated shapes (column block C, da): RBF C in {1, 2, 4, 8} with da <= 24 and
+// {11, 17, 33} with da <= 32; Matern-5/2 C in {11, 17} with da <= 16.  Any c up to the largest
+// runs on the next instantiation with zero-padded columns (the padded columns add no work to the
+// MUFU-bound pair loop, only to the int8 MMAs).
+int k1tc2_cols(int kind, int d, int c) {
     const int da = tc2_da(d);
-    if (kind == BBMM_MATERN52) return (c == 17 || c == 11) && da <= 16;   // MODE 2 instantiations
-    if (kind != BBMM_RBF) return false;
-    switch (c) {
-        case 1: case 2: case 4: case 8: return da <= 24;
-        case 11: case 17: case 33: return da <= 32;
-        default: return false;
-    }
+    if (kind == BBMM_MATERN52) return da > 16 ? 0 : c <= 11 ? 11 : c <= 17 ? 17 : 0;
+    if (kind != BBMM_RBF || da > 32) return 0;
+    if (da <= 24)
+        for (int v : {1, 2, 4, 8})
+            if (c <= v) return v;
+    return c <= 11 ? 11 : c <= 17 ? 17 : c <= 33 ? 33 : 0;
+}
+bool k1tc2_supported(int kind, int d, int c) { return k1tc2_cols(kind, d, c) > 0; }
+// isotropic-RBF derivative (MODE 1) instantiations: C in {11, 17, 33}, any da <= 32
+int k1tc2_deriv_cols(int d, int c) {
+    if (tc2_da(d) > 32) return 0;
+    return c <= 11 ? 11 : c <= 17 ? 17 : c <= 33 ? 33 : 0;
 }
 
 int64_t k1tc2_xa_floats(int64_t npad, int d) { return npad * tc2_da(d); }
@@ -676,9 +685,7 @@ size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c) {
 }
 
 bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c) {
-    // the instantiated derivative shapes (k1tc2_matmul, mode 1)
-    const int da = tc2_da(d);
-    return n_ls == 1 && kind == BBMM_RBF && ((c == 11 && da <= 24) || (c == 17 && da == 8));
+    return n_ls == 1 && kind == BBMM_RBF && k1tc2_deriv_cols(d, c) > 0;
 }
 
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
@@ -688,13 +695,15 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
     int sp = 1;
     const int da = tc2_da(d);
     if (mode == 1) {
-        BBMM_REQUIRE(k1tc2_deriv_supported(BBMM_RBF, 1, d, c), "k1tc2: derivative mode shape");
+        BBMM_REQUIRE(k1tc2_deriv_cols(d, c) == c, "k1tc2: derivative mode shape");
         if (nloc > 0) {
-            if (c == 11 && da == 8) sp = launch_tc2<11, 8, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 11 && da == 24) sp = launch_tc2<11, 24, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported derivative shape"};
+#define BBMM_TC2D(CC, DD) \
+    if (c == CC && da == DD) sp = launch_tc2<CC, DD, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+            BBMM_TC2D(11, 8) BBMM_TC2D(11, 16) BBMM_TC2D(11, 24) BBMM_TC2D(11, 32)
+            BBMM_TC2D(17, 8) BBMM_TC2D(17, 16) BBMM_TC2D(17, 24) BBMM_TC2D(17, 32)
+            BBMM_TC2D(33, 8) BBMM_TC2D(33, 16) BBMM_TC2D(33, 24) BBMM_TC2D(33, 32)
+            throw Error{BBMM_ERR_ARG, "k1tc2: unsupported derivative shape"};
+#undef BBMM_TC2D
         }
         if (ev1) record_event(ctx, ev1);
         return sp;
@@ -745,19 +754,21 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         op.version = 2;
         op.kind = h.kind;
         op.nd = h.kind == BBMM_MATERN52 ? 5 : 4;
+        op.cb = k1tc2_cols(h.kind, d, c);
         op.Xa = xa;
         op.XB = xb;
     }
     return op;
 }
 
-size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int c) {
-    return op.version == 3 ? k2tc_vpart_elems(n, nloc, c) : k1tc2_vpart_elems(n, nloc, c);
+size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int cb) {
+    return op.version == 3 ? k2tc_vpart_elems(n, nloc, cb) : k1tc2_vpart_elems(n, nloc, cb);
 }
 
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
               int64_t n, int64_t r0, int64_t nloc, double s, double *Vpart, size_t cap,
               cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
+    // c = the column block (instantiation) to run; Bp packed for it
     if (op.version == 3) {
         BBMM_REQUIRE(mode == 0, "k2tc: stored K has no derivative mode");
         return k2tc_matmul(ctx, op.Kq, Bp, S, c, n, nloc, s, Vpart, cap, ev0, ev1);

@@ -389,12 +389,13 @@ static int launch(bbmm_ctx_s *ctx, const uint8_t *Kq, const uint8_t *Bp, const d
 // ======================================================================
 // host side
 // ======================================================================
-bool k2tc_supported(int c) {
-    switch (c) {
-        case 1: case 2: case 4: case 8: case 11: case 16: case 17: case 32: case 33: return true;
-        default: return false;
-    }
+// instantiated column counts; any c up to 33 runs on the next one (zero-padded columns)
+int k2tc_cols(int c) {
+    for (int v : {1, 2, 4, 8, 11, 16, 17, 32, 33})
+        if (c <= v) return v;
+    return 0;
 }
+bool k2tc_supported(int c) { return k2tc_cols(c) > 0; }
 
 size_t k2tc_vpart_elems(int64_t n, int64_t nloc, int c) {
     const k2tc::Plan p = k2tc::plan(nloc, k1tc_pad_rows(n));
@@ -439,6 +440,7 @@ TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const f
         op.d = d;
         op.kind = h.kind;
         op.nd = k2tc::ND;
+        op.cb = k2tc_cols(c);
         op.Kq = kq;
         return op;
     }

@@ -749,10 +749,12 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     const bool use_sor = a.sor_B != nullptr;
     const bool use_tc = a.tc.version != 0 && !use_sor;
     size_t vcap = use_sor ? (size_t)std::max<int64_t>(nloc, 1) * cs
-                 : use_tc ? tc_vpart_elems(a.tc, a.n, nloc, c) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
+                 : use_tc ? tc_vpart_elems(a.tc, a.n, nloc, a.tc.cb) : vpart_elems(a.n, nloc, cp, a.Kst != nullptr);
     const int64_t npad_tc = use_tc ? k1tc_pad_rows(npad) : 0;
     const int tc_nd = use_tc ? tc_dslices(a.tc) : 4;
-    const int tc_rows = tc_bslice_rows(c, tc_nd);
+    const int cb = use_tc ? a.tc.cb : c;              // columns of the tensor-core instantiation
+    const int tc_rows = tc_bslice_rows(cb, tc_nd);
+    const int vs = use_tc ? tc_vstride(a.tc) : cs;    // Vpart row stride
     uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * tc_rows) : nullptr;
     double *Stc = use_tc ? (double *)ws.get("tc_S", kMaxCols * 8) : nullptr;
     if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, (size_t)npad_tc * tc_rows, sm));
@@ -899,7 +901,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             // tensor-core operand: global column scales, then int8 slices
             k1tc_colmax(ctx, D, c, nloc, c, Stc);
             if (multi) allreduce_max(ctx, Stc, c);
-            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp, tc_nd);
+            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp, tc_nd, cb);
             if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * tc_rows);
         } else if (multi && !use_sor) {          // SoR needs only local rows of D
             allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
@@ -936,7 +938,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         if (use_sor)
             splits = sor_matmul(e0, e1);
         else if (use_tc)
-            splits = tc_matmul(ctx, a.tc, Bp, Stc, c, a.n, a.r0, nloc, a.s, Vpart, vcap, e0, e1);
+            splits = tc_matmul(ctx, a.tc, Bp, Stc, cb, a.n, a.r0, nloc, a.s, Vpart, vcap, e0, e1);
         else if (a.Kst)
             splits = kernel_matmul_stored(ctx, a.Kst, a.n, nloc, Dm, acc64, cp, Vpart, vcap, e0,
                                           e1);
@@ -944,13 +946,13 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             splits = kernel_matmul_onthefly(ctx, a.kind, a.Xs, a.dp, a.n, a.r0, nloc, Dm, acc64,
                                             cp, a.s, Vpart, vcap, e0, e1);
         if (fused) {
-            FusedIo io{st, Vpart, splits, cs, c, k, nloc, a.n, a.noise_var, a.tol, D, V, U, R, Z,
+            FusedIo io{st, Vpart, splits, vs, c, k, nloc, a.n, a.noise_var, a.tol, D, V, U, R, Z,
                        a.L, Cinv, ahist, bhist, rhist, fpart, fpartW, fred, Dm, acc64 ? 0 : 1,
                        use_tc ? Bp : nullptr, tc_nd, tc_rows, Stc,
-                       use_tc ? k1tc_pad_rows(a.n) : 0};
+                       use_tc ? k1tc_pad_rows(a.n) : 0, cb};
             mbcg_fused_iteration(ctx, fplan, io);
         } else {
-            k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, cs, nloc, c, a.noise_var, D, V, part);
+            k_passA<<<g.grid, g.block, 0, sm>>>(Vpart, splits, vs, nloc, c, a.noise_var, D, V, part);
             reduce(c, red);
             if (multi) allreduce_sum(ctx, red, c);
             k_alpha<<<1, 64, 0, sm>>>(st, red, ahist, c);

@@ -57,6 +57,7 @@ struct Args {
     uint8_t *Bp;
     double *Stc;
     int64_t pad_end;   // points covered by Bp (k1tc_pad_rows(n))
+    int cb;            // instantiation columns: D in [0, c), zero D in [c, cb), constant at cb
     int KT;
 };
 
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kT, 1) k_mbcg_fused(Args a) {
             const int64_t q = q0 + e / a.nb_rows;
             const int bi = nn / a.blk_cols, col = nn - bi * a.blk_cols;
             uint32_t wv[4] = {0, 0, 0, 0};
-            if (bi < a.nd && col <= c) {
+            if (bi < a.nd && col <= a.cb) {
                 const int shift = 8 * (a.nd - 1 - bi);
 #pragma unroll 4
                 for (int p = 0; p < 16; p++) {
@@ -480,6 +481,7 @@ void mbcg_fused_iteration(bbmm_ctx_s *ctx, const FusedPlan &p, const FusedIo &io
     a.Dm = io.Dm; a.dm_f32 = io.dm_f32;
     a.use_tc = io.Bp != nullptr; a.nd = io.nd; a.blk_cols = io.nb_rows / std::max(io.nd, 1);
     a.nb_rows = io.nb_rows; a.Bp = io.Bp; a.Stc = io.Stc; a.pad_end = io.pad_end; a.KT = p.KT;
+    a.cb = io.cb > 0 ? io.cb : io.c;
     void *args[] = {&a};
     BBMM_CUDA(cudaLaunchCooperativeKernel(p.fn, dim3(p.G), dim3(fz::kT), args, p.smem, ctx->stream));
     ctx->launches++;
