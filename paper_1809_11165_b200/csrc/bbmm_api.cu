@@ -668,10 +668,22 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             }
             allgather_rows(ctx, B32, (size_t)rr.nb * cs * 4);
             const bool dtc = ctx->matmul_tc && deriv_tc_supported(h.kind, dp, cp, n);
+            // RBF ARD with the K1-TC operand: the expanded-square tensor-core pass
+            const bool dtc2 = ctx->matmul_tc && tcop.version == 2 &&
+                              deriv_tc2_supported(h.kind, h.n_ls, d, dp, c, n);
             double *dpart = (double *)ws.get(
-                "d_part", std::max(derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp),
-                                   deriv_tc_part_elems(n, std::max<int64_t>(nloc, 1), dp)) * 8);
-            if (nloc > 0) {
+                "d_part", std::max({derivative_part_elems(n, std::max<int64_t>(nloc, 1), dp),
+                                    deriv_tc_part_elems(n, std::max<int64_t>(nloc, 1), dp),
+                                    deriv_tc2_part_elems(n, std::max<int64_t>(nloc, 1), dp)}) * 8);
+            if (dtc2) {
+                derivative_pass_tc2(ctx, tcop.Xa, d, dp, n, rr.r0, nloc, A32, B32, cs, c, o.U_d,
+                                    o.R_d, B, Z0, h.noise_var, h.s, dpart, dred);
+                if (nloc > 0) {
+                    k_scalar_terms<<<sblk, 256, 0, sm>>>(o.U_d, Z0, y, rr.r0, nloc, t, spart);
+                    ctx->launches++;
+                    reduce_blocks(ctx, spart, sblk, 3, dred + nq);
+                }
+            } else if (nloc > 0) {
                 int nblk = 0;
                 if (dtc)   // W tiles on the tensor cores (deriv_tc.cu)
                     nblk = derivative_pass_tc(ctx, h.kind, Xs, dp, n, rr.r0, nloc, A32, B32, cp, c,

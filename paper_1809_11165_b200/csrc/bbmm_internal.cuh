@@ -353,6 +353,13 @@ int derivative_pass_tc(bbmm_ctx_s *ctx, int kind, const float *Xs, int dp, int64
                        int64_t nloc, const float *A32, const float *B32, int cp, int c,
                        double *part);
 void reduce_blocks(bbmm_ctx_s *ctx, const double *part, int nblk, int m, double *red);
+// deriv_tc2.cu: the RBF-ARD derivative as tensor-core products (expanded square, M = k~ o W)
+bool deriv_tc2_supported(int kind, int n_ls, int d, int dp, int c, int64_t n);
+size_t deriv_tc2_part_elems(int64_t n, int64_t nloc, int dp);
+void derivative_pass_tc2(bbmm_ctx_s *ctx, const float *Xa, int d, int dp, int64_t n, int64_t r0,
+                         int64_t nloc, const float *A32, const float *B32, int cs, int c,
+                         const double *U, const double *R, const double *Bblk, const double *Z0,
+                         double noise_var, double s, double *part, double *red);
 
 // ------------------------------------------------------------- comm
 // A context communicates when it has an NCCL communicator (also a 1-rank one, which issues
