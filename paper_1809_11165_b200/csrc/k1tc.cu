@@ -16,13 +16,7 @@ namespace bbmm {
 
 namespace tc {
 
-constexpr int BM = 128;
-constexpr int BK = 64;
-constexpr int STAGES = 3;
-constexpr int WINDOW = 16384;                 // j per TMEM drain (int32 bound)
-constexpr int kThreads = 192;
-constexpr __host__ __device__ int round16(int x) { return (x + 15) & ~15; }
-constexpr __host__ __device__ int round32(int x) { return (x + 31) & ~31; }
+constexpr int BK = 64;                        // points per packed chunk group (16-point chunks)
 
 __global__ void k_col_mean(const float *__restrict__ X, int64_t n, int d, double *__restrict__ mean) {
     const int q = blockIdx.x;

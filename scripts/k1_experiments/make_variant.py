@@ -1,173 +1,29 @@
-"""Scratch: build a libbbmm variant with extra -D flags for k1tc2.cu.
-usage: python scratch/make_variant.py NAME -DFOO=1 ..."""
-import os, shutil, subprocess, sys
+"""Build a libbbmm variant whose k1tc2.cu is compiled with extra -D flags (timing experiments).
+
+    python scripts/k1_experiments/make_variant.py NAME -DBBMM_TC2_NPS=6 ...
+
+Writes scratch/var_NAME/paper_1809_11165_b200/lib/libbbmm.so (the other objects from the main
+build); time it with scripts/k1_ab.py.  Source ablations: ablate.py."""
+import os
+import shutil
+import subprocess
+import sys
+
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-from paper_1809_11165_b200 import _build as B
-name, defs = sys.argv[1], [a for a in sys.argv[2:] if a != "--only-c4"]
-only_c4 = "--only-c4" in sys.argv
+from paper_1809_11165_b200 import _build as B  # noqa: E402
+
+name, defs = sys.argv[1], sys.argv[2:]
 inc, libdir = B.nccl_paths()
 objs = [os.path.join(B.BUILD, f) for f in os.listdir(B.BUILD) if f.endswith(".o") and f != "k1tc2.cu.o"]
 d = os.path.join(ROOT, "scratch", "var_" + name, "paper_1809_11165_b200")
 os.makedirs(os.path.join(d, "lib"), exist_ok=True)
 shutil.copy(os.path.join(ROOT, "paper_1809_11165_b200", "__init__.py"), d)
 o = os.path.join(ROOT, "scratch", "var_" + name, "k1tc2.o")
-src = open(os.path.join(B.CSRC, "k1tc2.cu")).read()
-if only_c4:   # instantiate only <17, 8> (tuning shapes whose smem ring does not fit the others)
-    import re
-    src = re.sub(r"BBMM_TC2\(1, 8\).*?BBMM_TC2\(11, 24\)", "BBMM_TC2(17, 8)", src, flags=re.S)
-    src = re.sub(r"if \(c == 11 && da == 8\)[^\n]*\n[^\n]*\n[^\n]*\n", "", src)
-    src = src.replace("else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 1>", "if (c == 17 && da == 8) sp = launch_tc2<17, 8, 1>")
-abl = os.environ.get("ABLATE", "")
-if "noi8" in abl:
-    src = src.replace("ptx::mma_i8_ts(tmem + 0, aq", "if (0) ptx::mma_i8_ts(tmem + 0, aq")
-    src = src.replace("ptx::mma_i8_ts(tmem + K::BLK, aq", "if (0) ptx::mma_i8_ts(tmem + K::BLK, aq")
-    src = src.replace("ptx::mma_i8_ts(tmem + 2 * K::BLK, aq", "if (0) ptx::mma_i8_ts(tmem + 2 * K::BLK, aq")
-if "q2only" in abl:
-    src = src.replace("ptx::mma_i8_ts(tmem + K::BLK, aq", "if (0) ptx::mma_i8_ts(tmem + K::BLK, aq")
-    src = src.replace("ptx::mma_i8_ts(tmem + 2 * K::BLK, aq", "if (0) ptx::mma_i8_ts(tmem + 2 * K::BLK, aq")
-if "nomufu" in abl:
-    src = src.replace("float kv = ex2_approx(sj);", "float kv = sj;")
-if "nosttm" in abl:
-    src = src.replace("ptx::tmem_st8(col + 0,", "if (0) ptx::tmem_st8(col + 0,").replace("ptx::tmem_st8(col + 8,", "if (0) ptx::tmem_st8(col + 8,").replace("ptx::tmem_st8(col + 16,", "if (0) ptx::tmem_st8(col + 16,")
-if "split" in abl:
-    a = """            if (t > 0) publish(t - 1);
-#pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            // overwrite own S columns with the A slices q0 | q1 | q2 (column maps above)
-            if constexpr (JW == 32) {
-                ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
-                ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
-                ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));
-            } else {"""
-    b = """            if (t > 0) publish(t - 1);
-            if constexpr (JW == 32) {
-                ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
-                ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
-                ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
-            }
-#pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            if constexpr (JW == 32) {
-                ptx::tmem_st4(col + 4, *reinterpret_cast<const uint32_t(*)[4]>(w0 + 4));
-                ptx::tmem_st4(col + 12, *reinterpret_cast<const uint32_t(*)[4]>(w1 + 4));
-                ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
-            } else {"""
-    assert a in src
-    src = src.replace(a, b)
-if "stx32" in abl:
-    a = """                ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
-                ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
-                ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));"""
-    b = """                asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
-                         ::"r"(col), "r"(w0[0]), "r"(w0[1]), "r"(w0[2]), "r"(w0[3]), "r"(w0[4]), "r"(w0[5]), "r"(w0[6]), "r"(w0[7]), "r"(w1[0]), "r"(w1[1]), "r"(w1[2]), "r"(w1[3]), "r"(w1[4]), "r"(w1[5]), "r"(w1[6]), "r"(w1[7]),
-                           "r"(w2[0]), "r"(w2[1]), "r"(w2[2]), "r"(w2[3]), "r"(w2[4]), "r"(w2[5]), "r"(w2[6]), "r"(w2[7]), "r"(w0[0]), "r"(w0[1]), "r"(w0[2]), "r"(w0[3]), "r"(w0[4]), "r"(w0[5]), "r"(w0[6]), "r"(w0[7]) : "memory");"""
-    assert a in src
-    src = src.replace(a, b)
-if "quarter" in abl:
-    a = """#pragma unroll
-            for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            if (t > 0) publish(t - 1);
-#pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            // overwrite own S columns with the A slices q0 | q1 | q2 (column maps above)
-            if constexpr (JW == 32) {
-                ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
-                ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
-                ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));
-            } else {"""
-    b = """            auto st2 = [&](uint32_t a, uint32_t x, uint32_t y) {
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(a), "r"(x), "r"(y) : "memory");
-            };
-#pragma unroll
-            for (int qq = 0; qq < 4; qq++) {
-                quant4(sv, 2 * qq, w0[2 * qq], w1[2 * qq], w2[2 * qq]);
-                quant4(sv, 2 * qq + 1, w0[2 * qq + 1], w1[2 * qq + 1], w2[2 * qq + 1]);
-                if (qq == 0 && t > 0) publish(t - 1);
-                st2(col + 2 * qq, w0[2 * qq], w0[2 * qq + 1]);
-                st2(col + 8 + 2 * qq, w1[2 * qq], w1[2 * qq + 1]);
-                st2(col + 16 + 2 * qq, w2[2 * qq], w2[2 * qq + 1]);
-            }
-            if constexpr (JW == 32) {
-            } else {"""
-    assert a in src
-    src = src.replace(a, b)
-if "ldfirst" in abl:
-    a = """        for (int t = 0; t < ntl; t++) {
-            const int b = t % K::NBUF;
-            ptx::mbar_wait_a(a_sfull + 8 * b, (uint32_t)((t / K::NBUF) & 1));
-            ptx::tc_fence_after();
-            uint32_t sv[JW];
-            const uint32_t col = my_col + b * BK;
-            if constexpr (JW == 32) {
-                ptx::tmem_ld32(col, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; u++) ptx::tmem_ld4(col + 8 * u, sv + 4 * u);
-            }
-            ptx::tmem_ld_wait();"""
-    b = """        uint32_t sv[JW];
-        if (ntl > 0) {
-            ptx::mbar_wait_a(a_sfull, 0);
-            ptx::tc_fence_after();
-            ptx::tmem_ld32(my_col, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            ptx::tmem_ld_wait();
-        }
-        for (int t = 0; t < ntl; t++) {
-            const int b = t % K::NBUF;
-            const uint32_t col = my_col + b * BK;"""
-    assert a in src
-    src = src.replace(a, b)
-    a = """#pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            if constexpr (JW == 32) {
-                ptx::tmem_st4(col + 4"""
-    b = """#pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
-            const bool more = t + 1 < ntl;
-            if (more) {
-                const int bn = (t + 1) % K::NBUF;
-                ptx::mbar_wait_a(a_sfull + 8 * bn, (uint32_t)(((t + 1) / K::NBUF) & 1));
-                ptx::tc_fence_after();
-                ptx::tmem_ld32(my_col + bn * BK, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            }
-            if constexpr (JW == 32) {
-                ptx::tmem_st4(col + 4"""
-    assert a in src
-    src = src.replace(a, b)
-    a = """                ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
-            } else {"""
-    b = """                ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
-                if (more) ptx::tmem_ld_wait();
-            } else {"""
-    assert a in src
-    src = src.replace(a, b)
-if "n16" in abl:
-    src = src.replace("constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);", "constexpr uint32_t IDQ = ptx::idesc_i8(BM, 16, false, false);")
-if "dist1" in abl or "dist2" in abl:
-    a = "for (int ks = 0; ks < 3 * DA / 8; ks++) {"
-    assert a in src
-    src = src.replace(a, "for (int ks = 0; ks < %d; ks++) {" % (1 if "dist1" in abl else 2))
-if "sttmlive" in abl:
-    # drop the A-slice stores but keep the quantised words live (no dead-code elimination)
-    for a_ in ("ptx::tmem_st4(col + 0,", "ptx::tmem_st4(col + 8,", "ptx::tmem_st4(col + 16,",
-               "ptx::tmem_st4(col + 4,", "ptx::tmem_st4(col + 12,", "ptx::tmem_st4(col + 20,"):
-        assert a_ in src, a_
-        src = src.replace(a_, "if (0) " + a_)
-    a_ = "            uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];"
-    assert a_ in src
-    src = src.replace(a_, a_ + "\n            uint32_t live_ = 0;")
-    a_ = "        if (ntl > 0) publish(ntl - 1);"
-    assert a_ in src
-    # fold every word into live_ at the end of each tile, store it only if impossible value
-    b_ = "            if constexpr (JW == 32) {\n                ptx::tmem_st4(col + 4"
-    src = src.replace("            if constexpr (JW == 32) {\n                if (0) ptx::tmem_st4(col + 4",
-                      "#pragma unroll\n            for (int u_ = 0; u_ < JW / 4; u_++) live_ ^= w0[u_] + w1[u_] * 3u + w2[u_] * 7u;\n            if (live_ == 0x9e3779b9u) Vpart[threadIdx.x] = (double)live_;\n            if constexpr (JW == 32) {\n                if (0) ptx::tmem_st4(col + 4")
-    assert "live_ ^=" in src
-f = os.path.join(ROOT, "scratch", "var_" + name, "k1tc2.cu")
-open(f, "w").write(src)
-subprocess.check_call([B.NVCC, "-std=c++17", "-O3", *B.ARCH, "-Xcompiler", "-fPIC", *defs, "-I", inc, "-I", B.CSRC,
-                       "-I", os.path.join(ROOT, "include"), "-c", f, "-o", o])
+subprocess.check_call([B.NVCC, "-std=c++17", "-O3", *B.ARCH, "-Xcompiler", "-fPIC", *defs, "-I", inc,
+                       "-I", B.CSRC, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
+                       "-c", os.path.join(B.CSRC, "k1tc2.cu"), "-o", o])
 subprocess.check_call([B.NVCC, "-shared", *B.ARCH, "-o", os.path.join(d, "lib", "libbbmm.so"), o, *objs,
                        "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"])
+os.remove(o)
 print("ok", name)
