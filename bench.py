@@ -45,8 +45,8 @@ def peaks():
 DTYPE = {
     0: "fp32 kernel values x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
     1: "stored fp32 K x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
-    2: "22-bit fixed-point k~ (3 u8 slices) x 31-bit fixed-point D (4 u8 slices), exact int32 "
-       "accumulation on tcgen05; fp64 CG",
+    2: "23-bit fixed-point k~ (3 u8 slices) x 31-bit fixed-point D (4 u8 slices; Matern 39-bit, "
+       "5 slices), exact int32 accumulation on tcgen05; fp64 CG",
     3: "stored 30-bit fixed-point K (4 u8 slices, fp64-built) x 55-bit fixed-point D (7 u8 slices), "
        "exact int32 accumulation on tcgen05; fp64 CG",
 }
