@@ -370,8 +370,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::fence_proxy_async_smem();
             ptx::tc_fence_before();
             ptx::mbar_arrive(&init_done);
-            for (int c = 0; c <= C; c++) acc_sm[c][rl] = 0.0;
         }
+        // each warp zeroes the fp64 sums it alone accumulates (columns cc = h mod NPS of its
+        // rows, drain_window): no cross-warp order needed before the first drain
+        for (int cc = h; cc <= C; cc += NPS) acc_sm[cc][sub * 32 + lane] = 0.0;
         const uint32_t a_sfull = ptx::smem_u32(&s_full[0]);
         const uint32_t a_afull = ptx::smem_u32(&a_full[0]);
         const uint32_t a_accf = ptx::smem_u32(&acc_full), a_acce = ptx::smem_u32(&acc_empty);
