@@ -263,6 +263,20 @@ bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X_d, const float *y_d,
                            bbmm_kmode_t kmode, int32_t k, int32_t max_iter,
                            double tol, double *mean_d, double *var_d);
 
+/* The full predictive (latent) covariance between the test points, Eq. 1
+ * with zero prior mean (reading R19):
+ *   cov[q][r] = k(x*_q, x*_r) - k_{X x*_q}^T Khat^{-1} k_{X x*_r}
+ * from the same batched mBCG solves as bbmm_predict (u_r = Khat^{-1} k_{X x*_r}); the
+ * contraction K_{*X} U_* runs over this rank's rows and is all-reduced.  Its diagonal is
+ * bbmm_predict's var.  Inputs as bbmm_predict, 1 <= nstar <= 8192.  Outputs (device, fp64,
+ * identical on every rank): mean_d (nstar), cov_d (nstar x nstar row-major).
+ * Errors: as bbmm_predict. */
+bbmm_status_t bbmm_predict_cov(bbmm_ctx_t ctx, const float *X_d, const float *y_d,
+                               int64_t n, int32_t d, const float *Xstar_d,
+                               int64_t nstar, const bbmm_hyper_t *hyper,
+                               bbmm_kmode_t kmode, int32_t k, int32_t max_iter,
+                               double tol, double *mean_d, double *cov_d);
+
 /* Hyperparameter training ("All methods use
  * the same optimizer (Adam)"; settings by DESIGN.md reading R26): `steps` Adam
  * steps on theta = (log l_1..l_{n_ls}, log s, log sigma) minimising -mll, with

@@ -99,6 +99,8 @@ def _declare(L):
     L.orc_num_threads.restype = _i
     L.orc_predict.argtypes = [_i, _p, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _i, _i, _d, _p, _p]
     L.orc_predict.restype = _i
+    L.orc_predict_cov.argtypes = [_i, _p, _p, _i64, _i, _p, _i64, _i, _p, _d, _d, _i, _i, _d, _p, _p]
+    L.orc_predict_cov.restype = _i
     L.orc_train_adam.argtypes = [_i, _p, _p, _i64, _i, _i, _p, _i, _i, _i, _d, _u64, _i, _d, _d,
                                  _d, _d, _p, _p]
     L.orc_train_adam.restype = _i
@@ -364,6 +366,22 @@ def predict(kind, X, y, Xstar, log_ls, log_s, log_noise, k, p, tol=0.0):
                              float(log_s), float(log_noise), k, p, float(tol), _ptr(mean),
                              _ptr(var)), "predict")
     return mean, var
+
+
+def predict_cov(kind, X, y, Xstar, log_ls, log_s, log_noise, k, p, tol=0.0):
+    """Predictive mean and the full latent covariance between the test points (Eq. 1,
+    PAPER.md:617-620; the oracle of bbmm_predict_cov).  Returns (mean (ns,), cov (ns, ns))."""
+    X = _f32(X)
+    n, d = X.shape
+    y = _f32(y)
+    Xs = _f32(np.asarray(Xstar).reshape(-1, d))
+    ns = Xs.shape[0]
+    lls = _f64(np.atleast_1d(log_ls))
+    mean, cov = np.zeros(ns), np.zeros((ns, ns))
+    _check(lib().orc_predict_cov(kind, _ptr(X), _ptr(y), n, d, _ptr(Xs), ns, lls.size, _ptr(lls),
+                                 float(log_s), float(log_noise), k, p, float(tol), _ptr(mean),
+                                 _ptr(cov)), "predict_cov")
+    return mean, cov
 
 
 # ------------------------------------------------------------ training

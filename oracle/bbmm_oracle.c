@@ -878,10 +878,37 @@ int orc_mll_and_grad(int kind, const float *X32, const float *y32, int64_t n,
 /* the rank-k pivoted-Cholesky preconditioner and no probes (SPEC "predict":   */
 /* "the n* solves performed as one batched mbcg call (probes absent)").       */
 /* ------------------------------------------------------------------------ */
+static int predict_core(int kind, const float *X32, const float *y32, int64_t n, int d,
+                        const float *Xs32, int64_t ns, int n_ls, const double *log_ls,
+                        double log_s, double log_noise, int k, int p, double tol,
+                        double *mean, double *var, double *cov);
+
 int orc_predict(int kind, const float *X32, const float *y32, int64_t n, int d,
                 const float *Xs32, int64_t ns, int n_ls, const double *log_ls,
                 double log_s, double log_noise, int k, int p, double tol,
                 double *mean, double *var)
+{
+    return predict_core(kind, X32, y32, n, d, Xs32, ns, n_ls, log_ls, log_s, log_noise, k, p,
+                        tol, mean, var, NULL);
+}
+
+/* The full predictive covariance between test points (Eq. 1, latent, R27):     */
+/*   cov(x*_q, x*_r) = k(x*_q, x*_r) - k_{X x*_q}^T Khat^{-1} k_{X x*_r}                    */
+/* from the same single mBCG call (u_r = the solve of column r); ns x ns row-major.       */
+int orc_predict_cov(int kind, const float *X32, const float *y32, int64_t n, int d,
+                    const float *Xs32, int64_t ns, int n_ls, const double *log_ls,
+                    double log_s, double log_noise, int k, int p, double tol,
+                    double *mean, double *cov)
+{
+    if (!cov) return ORC_ERR_ARG;
+    return predict_core(kind, X32, y32, n, d, Xs32, ns, n_ls, log_ls, log_s, log_noise, k, p,
+                        tol, mean, NULL, cov);
+}
+
+static int predict_core(int kind, const float *X32, const float *y32, int64_t n, int d,
+                        const float *Xs32, int64_t ns, int n_ls, const double *log_ls,
+                        double log_s, double log_noise, int k, int p, double tol,
+                        double *mean, double *var, double *cov)
 {
     hyper_t h;
     if (n < 1 || ns < 1 || p < 1 || k < 0 || k > n || tol < 0) return ORC_ERR_ARG;
@@ -930,6 +957,16 @@ int orc_predict(int kind, const float *X32, const float *y32, int64_t n, int d,
             mean[q] = m;
             if (var)
                 var[q] = orc_kernel(kind, d, Xs + q * d, Xs + q * d, h.n_ls, h.ls, h.s) - v;
+        }
+        if (cov) {
+#pragma omp parallel for schedule(static)
+            for (int64_t q = 0; q < ns; q++)
+                for (int64_t r = 0; r < ns; r++) {
+                    double g = 0.0;
+                    for (int64_t i = 0; i < n; i++) g += B[i * c + 1 + q] * U[i * c + 1 + r];
+                    cov[q * ns + r] =
+                        orc_kernel(kind, d, Xs + q * d, Xs + r * d, h.n_ls, h.ls, h.s) - g;
+                }
         }
     }
     free(X); free(Xs); free(L); free(piv); free(cholC); free(B); free(U); free(al);

@@ -84,6 +84,8 @@ _lib.bbmm_mbcg.argtypes = [_p, _p, _i64, _i32, _HP, C.c_int, _p, _i32, _p, _i32,
 _lib.bbmm_mll_and_grad.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d,
                                    _u64, _p, C.POINTER(_d), _p, C.POINTER(Stats), _p, _p]
 _lib.bbmm_predict.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d, _p, _p]
+_lib.bbmm_predict_cov.argtypes = [_p, _p, _p, _i64, _i32, _p, _i64, _HP, C.c_int, _i32, _i32, _d,
+                                  _p, _p]
 _lib.bbmm_train_adam.argtypes = [_p, _p, _p, _i64, _i32, _HP, C.c_int, _i32, _i32, _i32, _d, _u64,
                                  _i32, _d, _d, _d, _d, _p, _p]
 _lib.bbmm_sor_mbcg.argtypes = [_p, _p, _i64, _i32, _p, _i32, _HP, _i32, _p, _i32, _i64, _i32, _d,
@@ -94,7 +96,8 @@ _lib.bbmm_ctx_set_local_comm.argtypes = [_p, _p, _i32]
 for _f in ("bbmm_local_group_create", "bbmm_local_group_destroy", "bbmm_ctx_set_local_comm",
            "bbmm_ctx_create", "bbmm_ctx_destroy", "bbmm_nccl_unique_id", "bbmm_ctx_set_comm",
            "bbmm_local_rows", "bbmm_ctx_set_matmul_precision", "bbmm_kernel_matmul", "bbmm_pivchol", "bbmm_mbcg",
-           "bbmm_mll_and_grad", "bbmm_predict", "bbmm_train_adam", "bbmm_sor_mbcg"):
+           "bbmm_mll_and_grad", "bbmm_predict", "bbmm_predict_cov", "bbmm_train_adam",
+           "bbmm_sor_mbcg"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -363,6 +366,26 @@ def predict(ctx: Context, X, y, Xstar, hyper: Hyper, k: int, max_iter: int = 20,
                                 max_iter, float(tol), _p(mean.data_ptr()),
                                 _p(var.data_ptr()) if var is not None else None))
     return mean, var
+
+
+def predict_cov(ctx: Context, X, y, Xstar, hyper: Hyper, k: int, max_iter: int = 20,
+                tol: float = 0.0, kmode: int = ONTHEFLY):
+    """GP predictive mean and the full latent covariance between the test points, Eq. 1
+    (bbmm_predict_cov).  Returns (mean (nstar,), cov (nstar, nstar)) as fp64 cuda tensors."""
+    torch = _torch()
+    n, d = _X_shape(X)
+    _shape(y, (n,), "y")
+    _shape(Xstar, (None, d), "Xstar")
+    ns = Xstar.shape[0]
+    mean = torch.empty(ns, dtype=torch.float64, device=X.device)
+    cov = torch.empty((ns, ns), dtype=torch.float64, device=X.device)
+    hp = hyper._c()
+    ctx.check(_lib.bbmm_predict_cov(ctx._h, _dev(X, torch.float32, "X", ctx),
+                                    _dev(y, torch.float32, "y", ctx), n, d,
+                                    _dev(Xstar, torch.float32, "Xstar", ctx), ns, C.byref(hp),
+                                    kmode, k, max_iter, float(tol), _p(mean.data_ptr()),
+                                    _p(cov.data_ptr())))
+    return mean, cov
 
 
 def train_adam(ctx: Context, X, y, hyper: Hyper, t: int, k: int, max_iter: int = 20,

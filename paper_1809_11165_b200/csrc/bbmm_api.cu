@@ -793,6 +793,29 @@ bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X, const float *y, int64
     });
 }
 
+bbmm_status_t bbmm_predict_cov(bbmm_ctx_t ctx, const float *X, const float *y, int64_t n,
+                               int32_t d, const float *Xstar, int64_t nstar,
+                               const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, int32_t k,
+                               int32_t max_iter, double tol, double *mean, double *cov) {
+    return guarded(ctx, [&] {
+        validate_common(ctx, X, n, d);
+        Hyper h = make_hyper(hyper, d);
+        BBMM_REQUIRE(y != nullptr && Xstar != nullptr && mean != nullptr && cov != nullptr,
+                     "y / Xstar / mean / cov is NULL");
+        BBMM_REQUIRE(nstar >= 1 && nstar <= kMaxPredCov, "nstar must be in [1, 8192]");
+        BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
+        BBMM_REQUIRE(max_iter >= 1 && max_iter <= 256, "max_iter must be in [1, 256]");
+        BBMM_REQUIRE(tol >= 0.0 && std::isfinite(tol), "tol must be >= 0");
+        BBMM_REQUIRE(kmode == BBMM_ONTHEFLY || kmode == BBMM_STORED, "bad kmode");
+        check_finite(ctx, X, n * d, "X");
+        check_finite(ctx, y, n, "y");
+        check_finite(ctx, Xstar, nstar * d, "Xstar");
+        predict_run(ctx, X, y, n, d, Xstar, nstar, h, kmode == BBMM_STORED, k, max_iter, tol, mean,
+                    nullptr, cov);
+        BBMM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X, const float *y, int64_t n,
                               int32_t d, const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, int32_t t,
                               int32_t k, int32_t max_iter, double tol, uint64_t seed, int32_t steps,

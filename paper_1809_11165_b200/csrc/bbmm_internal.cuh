@@ -19,6 +19,7 @@ constexpr int kMaxCols = 64;     // ncols = t + 1 <= 64
 constexpr int kMaxInducing = 512;  // SoR operator: inducing points m (row f4)
 constexpr int kMaxRank = 128;    // preconditioner rank k
 constexpr int kMaxDim = 32;      // input dimension d
+constexpr int64_t kMaxPredCov = 8192;   // test points of bbmm_predict_cov (cov is nstar^2)
 constexpr int kNumSMs = 148;
 // bbmm_stats_t.unconverged: relres at exit above which mBCG counts as unconverged (SURVEY.md §8c
 // regime B; regime A runs end at <= 1e-6, the regime-B configs at 1e-2..0.2)
@@ -298,7 +299,7 @@ void pivchol_sor(bbmm_ctx_s *ctx, const double *Bs, int64_t n, int m, double s, 
 // predict.cu: mean and pointwise variance (var may be null)
 void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
                  const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,
-                 int max_iter, double tol, double *mean, double *var);
+                 int max_iter, double tol, double *mean, double *var, double *cov = nullptr);
 // mbcg_fused.cu: one cooperative kernel per iteration for the vector work (single rank)
 struct FusedPlan {
     bool ok = false;

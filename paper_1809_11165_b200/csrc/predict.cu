@@ -110,6 +110,66 @@ __global__ void k_pred_finish(const double *__restrict__ red, int m, double s, i
     }
 }
 
+// dst[i * ldd + dcol0 + q] = src[i * lds + scol0 + q]  (q < m)
+__global__ void k_copy_cols(const double *__restrict__ src, int lds, int scol0, int m,
+                            int64_t nloc, double *__restrict__ dst, int64_t ldd, int64_t dcol0) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nloc * m;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / m;
+        const int q = (int)(e - i * m);
+        dst[i * ldd + dcol0 + q] = src[i * lds + scol0 + q];
+    }
+}
+
+// G[q][r] = sum_i Kq[i][q] U[i][r] over the local rows (ns x ns, fp64): 16 x 16 output tiles,
+// 32-row chunks of both operands staged in shared memory, fixed summation order.
+__global__ void __launch_bounds__(256)
+k_gram(const double *__restrict__ Kq, const double *__restrict__ U, int64_t ns, int64_t nloc,
+       double *__restrict__ G) {
+    __shared__ double ka[32][17], ub[32][17];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t q = (int64_t)blockIdx.y * 16 + ty, r = (int64_t)blockIdx.x * 16 + tx;
+    double acc = 0.0;
+    for (int64_t i0 = 0; i0 < nloc; i0 += 32) {
+        for (int e = threadIdx.x; e < 32 * 16; e += 256) {
+            const int ii = e >> 4, c = e & 15;
+            const int64_t i = i0 + ii;
+            const int64_t qq = (int64_t)blockIdx.y * 16 + c, rr = (int64_t)blockIdx.x * 16 + c;
+            ka[ii][c] = (i < nloc && qq < ns) ? Kq[i * ns + qq] : 0.0;
+            ub[ii][c] = (i < nloc && rr < ns) ? U[i * ns + rr] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int ii = 0; ii < 32; ii++) acc = fma(ka[ii][ty], ub[ii][tx], acc);
+        __syncthreads();
+    }
+    if (q < ns && r < ns) G[q * ns + r] = acc;
+}
+
+// cov[q][r] = k(x*_q, x*_r) - G[q][r], kernel values in fp64 from the raw inputs
+__global__ void k_cov_finish(int kind, const float *__restrict__ Xs, int d, int64_t ns,
+                             const double *__restrict__ inv_ls2, double s,
+                             const double *__restrict__ G, double *__restrict__ cov) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns * ns;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / ns, r = e - q * ns;
+        const float *a = Xs + q * d, *b = Xs + r * d;
+        double r2 = 0.0;
+        for (int t = 0; t < d; t++) {
+            const double df = (double)a[t] - (double)b[t];
+            r2 += df * df * inv_ls2[t];
+        }
+        double kv;
+        if (kind == BBMM_RBF) {
+            kv = s * exp(-0.5 * r2);
+        } else {
+            const double rr = sqrt(r2), sr = sqrt(5.0) * rr;
+            kv = s * (1.0 + sr + (5.0 / 3.0) * r2) * exp(-sr);
+        }
+        cov[e] = kv - G[e];
+    }
+}
+
 int pgrid(int64_t work) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), 8 * kNumSMs));
 }
@@ -118,7 +178,7 @@ int pgrid(int64_t work) {
 
 void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int d,
                  const float *Xstar, int64_t nstar, const Hyper &h, bool stored, int k,
-                 int max_iter, double tol, double *mean, double *var) {
+                 int max_iter, double tol, double *mean, double *var, double *cov) {
     cudaStream_t sm = ctx->stream;
     Workspace &ws = ctx->ws;
     constexpr int CW = kPredMaxM;                  // right-hand sides per mBCG call
@@ -176,13 +236,24 @@ void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int
         ctx->launches++;
     };
 
-    // batch 0: [y | first test columns] (variance) or [y] alone (mean only)
+    // covariance: keep every test column k_{X x*_q} and its solve (local rows x nstar)
+    const bool solves = var != nullptr || cov != nullptr;
+    double *Kq = cov ? (double *)ws.get("pred_Kq", (size_t)nl1 * nstar * 8) : nullptr;
+    double *Ust = cov ? (double *)ws.get("pred_Ust", (size_t)nl1 * nstar * 8) : nullptr;
+    auto keep = [&](const double *U, int col0, int m, int64_t q0) {
+        if (!cov || nloc == 0 || m == 0) return;
+        k_copy_cols<<<pgrid(nloc * m), 256, 0, sm>>>(B, CW, col0, m, nloc, Kq, nstar, q0);
+        k_copy_cols<<<pgrid(nloc * m), 256, 0, sm>>>(U, CW, col0, m, nloc, Ust, nstar, q0);
+        ctx->launches += 2;
+    };
+
+    // batch 0: [y | first test columns] (variance / covariance) or [y] alone (mean only)
     BBMM_CUDA(cudaMemsetAsync(B, 0, (size_t)nl1 * CW * 8, sm));
     if (nloc > 0) {
         k_y_col<<<pgrid(nloc), 256, 0, sm>>>(y, rr.r0, nloc, B, CW);
         ctx->launches++;
     }
-    const int m0 = var ? (int)std::min<int64_t>(nstar, CW - 1) : 0;
+    const int m0 = solves ? (int)std::min<int64_t>(nstar, CW - 1) : 0;
     cross(0, m0, 1);
     MbcgOut o;
     mbcg_run(ctx, a, B, CW, cholC, o);
@@ -190,8 +261,11 @@ void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int
         k_take_col<<<pgrid(nloc), 256, 0, sm>>>(o.U_d, CW, nloc, alpha);
         ctx->launches++;
     }
-    if (var) {
-        if (m0 > 0) dots(o.U_d, 1, m0, 0);
+    if (solves) {
+        if (m0 > 0) {
+            dots(o.U_d, 1, m0, 0);
+            keep(o.U_d, 1, m0, 0);
+        }
         // later batches: CW test columns each, solved together
         for (int64_t q0 = m0; q0 < nstar; q0 += CW) {
             const int m = (int)std::min<int64_t>(nstar - q0, CW);
@@ -200,6 +274,21 @@ void predict_run(bbmm_ctx_s *ctx, const float *X, const float *y, int64_t n, int
             MbcgOut ob;
             mbcg_run(ctx, a, B, CW, cholC, ob);
             dots(ob.U_d, 0, m, q0);
+            keep(ob.U_d, 0, m, q0);
+        }
+        if (cov) {
+            double *G = (double *)ws.get("pred_G", (size_t)nstar * nstar * 8);
+            if (nloc > 0) {
+                const dim3 gg((unsigned)ceil_div(nstar, 16), (unsigned)ceil_div(nstar, 16));
+                k_gram<<<gg, 256, 0, sm>>>(Kq, Ust, nstar, nloc, G);
+                ctx->launches++;
+            } else {
+                BBMM_CUDA(cudaMemsetAsync(G, 0, (size_t)nstar * nstar * 8, sm));
+            }
+            allreduce_sum(ctx, G, (size_t)nstar * nstar);
+            k_cov_finish<<<pgrid(nstar * nstar), 256, 0, sm>>>(h.kind, Xstar, d, nstar, inv_d,
+                                                               h.s, G, cov);
+            ctx->launches++;
         }
     } else {
         // mean only: k_{X x*}^T alpha, no further solves

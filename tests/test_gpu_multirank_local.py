@@ -258,3 +258,20 @@ def test_graph_capture_matches_eager_iterations(orc):
     np.testing.assert_array_equal(a["grad"], b["grad"])
     np.testing.assert_array_equal(a["U"].cpu().numpy(), b["U"].cpu().numpy())
     assert a["stats"]["ms_matmul"] > 0 and a["stats"]["matmul_launches"] == cfg.p
+
+
+def test_predict_cov_partitioned_matches_single_rank(orc):
+    cfg = synth.scaled(synth.CONFIGS["C4"], 3000)
+    pr = synth.make_problem(cfg, seed=0)
+    Xs = dev(synth.test_points(cfg, 21, seed=3))
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        m, C = bb.predict_cov(ctx, X, y, Xs, h, cfg.k, max_iter=cfg.p)
+        return m.cpu().numpy(), C.cpu().numpy()
+
+    parts = run_ranks(3, call)
+    m1, C1 = single(call)
+    for m, C in parts:
+        np.testing.assert_array_equal(C, parts[0][1])
+        assert np.abs(C - C1).max() <= 1e-8 and np.abs(m - m1).max() <= 1e-8

@@ -82,3 +82,23 @@ def test_predict_bad_args(ctx):
         bb.predict(ctx, X, y, dev(np.zeros((3, 3), np.float32)), h, 2)
     with pytest.raises(bb.BBMMError):
         bb.predict(ctx, X, y, dev(np.full((2, 2), np.nan, np.float32)), h, 2)
+
+
+@pytest.mark.parametrize("name,n,ns,kmode", [("C4", 3000, 40, bb.ONTHEFLY), ("C1", 2000, 17, bb.STORED),
+                                             ("C2", 1500, 5, bb.ONTHEFLY), ("C0", 256, 1, bb.ONTHEFLY)])
+def test_predict_cov_matches_oracle(ctx, orc, name, n, ns, kmode):
+    """Full predictive covariance between the test points (Eq. 1, bbmm_predict_cov) vs the
+    oracle's: element-wise 1e-4 s; its diagonal equals bbmm_predict's variance."""
+    cfg = synth.scaled(synth.CONFIGS[name], n)
+    pr = synth.make_problem(cfg, seed=5)
+    Xs = synth.test_points(cfg, ns, seed=9)
+    h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
+    k = min(cfg.k, n)
+    m, C = bb.predict_cov(ctx, dev(pr.X), dev(pr.y), dev(Xs), h, k, max_iter=cfg.p, kmode=kmode)
+    m, C = m.cpu().numpy(), C.cpu().numpy()
+    mo, Co = orc.predict_cov(cfg.kind, pr.X, pr.y, Xs, pr.log_ls, pr.log_s, pr.log_noise, k, cfg.p)
+    s = math.exp(pr.log_s)
+    assert np.abs(m - mo).max() <= 1e-4 * max(np.abs(mo).max(), 1e-3)
+    assert np.abs(C - Co).max() <= 1e-4 * s, float(np.abs(C - Co).max())
+    _, v = bb.predict(ctx, dev(pr.X), dev(pr.y), dev(Xs), h, k, max_iter=cfg.p, kmode=kmode)
+    np.testing.assert_allclose(np.diag(C), v.cpu().numpy(), rtol=0, atol=1e-12 * s)

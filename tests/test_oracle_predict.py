@@ -82,3 +82,37 @@ def test_mean_linear_in_y(orc):
     ysum_err = (y1.astype(np.float64) + y2) - (y1 + y2).astype(np.float32)
     assert np.abs(ysum_err).max() < 1e-6
     np.testing.assert_allclose(mc, ma + mb, atol=1e-6)
+
+
+def dense_cov(kind, X, Xs, log_ls, log_s, log_noise):
+    """K_{**} - K_{*X} Khat^{-1} K_{X*} via Cholesky (the textbook GP posterior covariance)."""
+    A = ref.khat(kind, X, log_ls, log_s, log_noise)
+    Ks = ref.kernel_matrix(kind, X, Xs, log_ls, log_s)
+    W = np.linalg.solve(np.linalg.cholesky(A), Ks)
+    return ref.kernel_matrix(kind, Xs, Xs, log_ls, log_s) - W.T @ W
+
+
+@pytest.mark.parametrize("kind,log_ls", [(ref.RBF, math.log(1.2)), (ref.MATERN52, np.log([0.9, 1.6]))])
+@pytest.mark.parametrize("k", [0, 5])
+def test_covariance_matches_dense_cholesky(orc, kind, log_ls, k):
+    """Full posterior covariance between test points (Eq. 1): the dense Cholesky formula at
+    p = n; its diagonal is the pointwise variance and the mean is unchanged."""
+    X, y, Xs = problem(ns=9)
+    m, C = orc.predict_cov(kind, X, y, Xs, log_ls, 0.2, math.log(0.3), k, 30, 1e-13)
+    Cd = dense_cov(kind, X.astype(np.float64), Xs.astype(np.float64), log_ls, 0.2, math.log(0.3))
+    np.testing.assert_allclose(C, Cd, rtol=0, atol=1e-9)
+    m2, v = orc.predict(kind, X, y, Xs, log_ls, 0.2, math.log(0.3), k, 30, 1e-13)
+    np.testing.assert_array_equal(m, m2)
+    np.testing.assert_allclose(np.diag(C), v, rtol=0, atol=1e-12)
+    assert np.min(np.linalg.eigvalsh(0.5 * (C + C.T))) > -1e-9     # PSD
+
+
+def test_covariance_of_coincident_points(orc):
+    """Two identical test points have covariance equal to their variance; far-apart test points
+    (no training data nearby) are uncorrelated."""
+    X, y, _ = problem()
+    Xs = np.array([[0.3, -0.2], [0.3, -0.2], [1e3, 1e3]], np.float32)
+    m, C = orc.predict_cov(ref.RBF, X, y, Xs, math.log(1.0), 0.0, math.log(0.2), 5, 30, 1e-13)
+    assert C[0, 1] == pytest.approx(C[0, 0], rel=1e-12)
+    assert C[0, 2] == pytest.approx(0.0, abs=1e-12)
+    assert C[2, 2] == pytest.approx(1.0, rel=1e-12)
