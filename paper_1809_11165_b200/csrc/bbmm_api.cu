@@ -424,6 +424,7 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
                                  const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, const double *D,
                                  int32_t ncols, int64_t ldd, double *V, int64_t ldv) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_kernel_matmul");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(D && V, "D / V is NULL");
@@ -489,6 +490,7 @@ bbmm_status_t bbmm_pivchol(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
                            const bbmm_hyper_t *hyper, int32_t k, double *L, int64_t *piv_h,
                            int32_t *k_used_h, double *resid_h) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_pivchol");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
@@ -509,6 +511,7 @@ bbmm_status_t bbmm_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d,
                         double *U, int64_t ldu, double *alpha_h, double *beta_h, int32_t *iters_h,
                         double *relres_h, double *rho0_h, double *relres_hist_h) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_mbcg");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(k >= 0 && k <= n && k <= kMaxRank, "k must be in [0, min(n, 128)]");
@@ -550,6 +553,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                                 const int8_t *eps, double *mll_h, double *grad_h,
                                 bbmm_stats_t *stats_h, double *U_out, int64_t *pivots_h) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_mll_and_grad");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(y != nullptr, "y is NULL");
@@ -565,6 +569,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         check_finite(ctx, y, n, "y");
         comm_timing_reset(ctx);
         Timer t_start(sm);
+        nv.next("pivchol");
         const int c = t + 1;
         RowRange rr = local_rows(ctx, n);
         const int64_t nloc = rr.count();
@@ -586,6 +591,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         BBMM_CUDA(cudaMemsetAsync(status, 0, sizeof(int), sm));
         precond_setup(ctx, L, n, k > 0 ? k_used : 0, h.noise_var, cholC, scal + 0);
         Timer t_pc(sm);
+        nv.next("mbcg");
 
         // 2. probes and B = [y | Z] (Eq. 3)
         double *B = (double *)ws.get("B", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
@@ -604,6 +610,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
         o.defer_host = true;                 // mbcg_finish after the final sync below
         mbcg_run(ctx, a, B, c, cholC, o);
         Timer t_cg(sm);
+        nv.next("slq");
 
         // 4. SLQ log-det (probe columns 1..t)
         const char *stb = reinterpret_cast<const char *>(o.state_d);
@@ -612,6 +619,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                    reinterpret_cast<const double *>(stb + offsetof(MbcgState, rho0)), max_iter, c,
                    1, t, scal + 1, status);
         Timer t_slq(sm);
+        nv.next("deriv");
 
         // 5. derivative pass (once)
         const int nq = dp + 1;
@@ -776,6 +784,7 @@ bbmm_status_t bbmm_predict(bbmm_ctx_t ctx, const float *X, const float *y, int64
                            bbmm_kmode_t kmode, int32_t k, int32_t max_iter, double tol,
                            double *mean, double *var) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_predict");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(y != nullptr && Xstar != nullptr && mean != nullptr, "y / Xstar / mean is NULL");
@@ -798,6 +807,7 @@ bbmm_status_t bbmm_predict_cov(bbmm_ctx_t ctx, const float *X, const float *y, i
                                const bbmm_hyper_t *hyper, bbmm_kmode_t kmode, int32_t k,
                                int32_t max_iter, double tol, double *mean, double *cov) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_predict_cov");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(y != nullptr && Xstar != nullptr && mean != nullptr && cov != nullptr,
@@ -822,6 +832,7 @@ bbmm_status_t bbmm_train_adam(bbmm_ctx_t ctx, const float *X, const float *y, in
                               double lr, double beta1, double beta2, double eps,
                               double *theta_out_h, double *trace_h) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_train_adam");
         validate_common(ctx, X, n, d);
         BBMM_REQUIRE(hyper != nullptr && hyper->log_ls_h != nullptr, "hyper is NULL");
         BBMM_REQUIRE(hyper->n_ls == 1 || hyper->n_ls == d, "n_ls must be 1 or d");
@@ -866,6 +877,7 @@ bbmm_status_t bbmm_sor_mbcg(bbmm_ctx_t ctx, const float *X, int64_t n, int32_t d
                             int64_t ldu, int64_t *piv_h, int32_t *iters_h, double *relres_h,
                             double *relres_hist_h) {
     return guarded(ctx, [&] {
+        NvtxPhase nv("bbmm_sor_mbcg");
         validate_common(ctx, X, n, d);
         Hyper h = make_hyper(hyper, d);
         BBMM_REQUIRE(Xu != nullptr && B != nullptr && U != nullptr, "Xu / B / U is NULL");

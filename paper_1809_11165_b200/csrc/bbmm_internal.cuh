@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <atomic>
@@ -66,6 +67,22 @@ struct Hyper {
     double s;            // outputscale
     double noise_var;    // sigma^2
     double sigma;
+};
+
+// NVTX ranges around the host-side phases of a call (visible to nsys / ncu --nvtx): one
+// range per entry point, next() closes the current phase and opens the following one.
+struct NvtxPhase {
+    int depth = 0;
+    explicit NvtxPhase(const char *call) { push(call); }
+    void next(const char *phase) {
+        if (depth > 1) { nvtxRangePop(); depth--; }
+        push(phase);
+    }
+    ~NvtxPhase() {
+        while (depth-- > 0) nvtxRangePop();
+    }
+  private:
+    void push(const char *name) { nvtxRangePushA(name); depth++; }
 };
 
 // ------------------------------------------------------------- workspace

@@ -1,12 +1,13 @@
 // k1tc2.cu -- Blackwell tensor-core kernel-matmul (K1-TC): V = s K~ D on the fly.
 //
 // The exact int8 contraction of DESIGN.md §6: kernel values k~ in [0, 1] as
-// 22-bit fixed point in three u8 slices (the low bytes of the fp32 q = 2 + k~),
+// 23-bit fixed point in three u8 slices (the low bytes of the fp32 q = 2 + 2 k~),
 // D as 31-bit (RBF) or 39-bit (Matern) fixed point per column (k1tc.cu), all
 // slice products on the int8 tensor cores with exact integer accumulation in
 // TMEM, drained to fp64.  Per 128 x 128 tile:
 //   * RBF (MODE 0 / 1): the exponent S_ij = -|xs_i - xs_j|^2 is itself a
-//     tcgen05 MMA (kind::tf32, 3xTF32 split) of augmented vectors
+//     tcgen05 MMA (3-product hi/lo split: kind::tf32 at d <= 6, kind::f16 with
+//     operands scaled by 2^5 above, half the MMAs there) of augmented vectors
 //       A_i = [2 xs_i, -|xs_i|^2, 1] (shared memory),  B_j = [xs_j, 1, -|xs_j|^2]
 //     (streamed [hi | lo] tiles) into a TMEM buffer; compute warps tcgen05.ld S,
 //     run ex2 on the MUFU (MODE 1: times r^2, the isotropic lengthscale
@@ -30,6 +31,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda_fp16.h>
+
 #include "bbmm_internal.cuh"
 #include "pair_common.cuh"
 #include "sm100_ptx.cuh"
@@ -37,17 +40,18 @@
 namespace bbmm {
 namespace tc2 {
 
-// j-tile BK = 96; 24 compute warps (6 per SM sub-partition, so that one
-// warp's barrier / TMEM latency is covered by the others' MUFU work), warp
-// (sub, h) serves TMEM lanes 32 sub.. and the j-group h (16 j) of every tile.
-// Each of the NBUF TMEM buffers (BK columns; NBUF = 4 when the accumulators
-// take <= 128 columns) first receives S (fp32, from the distance MMA); every
-// warp then overwrites 12 of ITS OWN 16 S columns with the three int8 slices
-// of its quantised kernel values, which the int8 MMAs read as A.  With three
-// buffers the MMA side runs two tiles ahead of the slowest warp.
+// j-tile BK = JW NPS (default 32 x 4 = 128); 4 NPS compute warps (NPS per SM
+// sub-partition, so that one warp's barrier / TMEM latency is covered by the
+// others' MUFU work), warp (sub, h) serves TMEM lanes 32 sub.. and the j-group
+// h (JW j) of every tile.  Each of the NBUF TMEM buffers (BK columns) first
+// receives S (fp32, from the distance MMA); every warp then overwrites 24 of
+// ITS OWN 32 S columns (JW = 32) with the three int8 slices of its quantised
+// kernel values, which the int8 MMAs read as A.  With three buffers the MMA
+// side runs two tiles ahead of the slowest warp.
 //
-// Column maps inside the 32-column group ks = h / 2 of a buffer (eo = h % 2,
-// u, v in 0..3, j' = 16 eo + 4 u + v the point's index within the group):
+// JW = 16 (a timing variant) column maps inside the 32-column group ks = h / 2
+// of a buffer (eo = h % 2, u, v in 0..3, j' = 16 eo + 4 u + v the point's index
+// within the group):
 //   S  of j'          -> column 8 u + 4 eo + v      (order of the B' rows)
 //   A  slice a, 4 j'  -> column 8 a + 4 eo + u      (K order = j', natural)
 // so the A columns a warp writes (u = 0..2 quarters) are among its own S
@@ -58,6 +62,16 @@ namespace tc2 {
 #ifndef BBMM_TC2_JW
 #define BBMM_TC2_JW 32
 #endif
+#ifndef BBMM_TC2_F16DIST
+#define BBMM_TC2_F16DIST 1
+#endif
+#ifndef BBMM_TC2_F16_MIN_DA
+#define BBMM_TC2_F16_MIN_DA 16
+#endif
+// fp16 distance operands are scaled by 2^5 (|xs|^2 by 2^10) so that the lo halves of the
+// split stay normal fp16 numbers down to |xs| ~ 2^-8 (the precision guard keeps |xs|^2 <= 16,
+// so 2^10 |xs|^2 <= 16384 < 65504); the MMA then yields 2^10 S, rescaled before ex2
+constexpr float kF16Scale = 32.0f;
 constexpr int NPS = BBMM_TC2_NPS;              // compute warps per lane quarter
 constexpr int JW = BBMM_TC2_JW;                // j per warp per tile (16 or 32)
 constexpr int BM = 128, BK = JW * NPS;         // j tile
@@ -109,9 +123,16 @@ struct Cfg {
     static constexpr int BUF_OFF = ACC_END;                    // NBUF x BK columns
     static constexpr int END = BUF_OFF + NBUF * BK;
     static_assert(END <= 512, "TMEM budget exceeded");
+    // Distance MMA operand type: kind::f16 (fp16 hi/lo split, K = 16 per MMA) when DA > 8 --
+    // half the MMAs of kind::tf32 (K = 8) at the same 11-bit split precision; at DA = 8 both
+    // take one MMA per product and tf32 stays (no operand scaling).  ND == 5 is Matern (MODE 2:
+    // plain fp32 x tiles, no distance MMA).
+    static constexpr bool F16 = BBMM_TC2_F16DIST && ND == 4 && DA >= BBMM_TC2_F16_MIN_DA;
+    static constexpr int DH = F16 ? r16(DA) : DA;              // K per product group
+    static constexpr int EB = F16 ? 2 : 4;                     // operand element bytes
     static constexpr int B8_BYTES = NB * BK;                   // int8 D slices per tile
-    static constexpr int XB_BYTES = 2 * DA * BK * 4;           // tf32 B' per tile: [hi | lo]
-    static constexpr int AP_BYTES = BM * 3 * DA * 4;           // row operand A' (smem)
+    static constexpr int XB_BYTES = 2 * DH * BK * EB;          // B' per tile: [hi | lo]
+    static constexpr int AP_BYTES = BM * 3 * DH * EB;          // row operand A' (smem)
     static constexpr int STATIC_BYTES = (C + 1) * BM * 8 + 512;   // acc_sm + barriers
     // Two shared-memory rings, each refilled as soon as its consumer MMA completes:
     // XB (read by the distance MMA of tile t, issued NBUF tiles before tile t's
@@ -259,7 +280,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // execute in issue order, so the distance MMA of tile t + K::NBUF, issued
         // right after the int8 MMAs of tile t that read the same TMEM buffer,
         // cannot overwrite it early: no buffer-free round trip is needed.
-        constexpr uint32_t IDS = ptx::idesc_tf32(BM, BK);
+        constexpr uint32_t IDS = K::F16 ? ptx::idesc_f16(BM, BK) : ptx::idesc_tf32(BM, BK);
         constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
@@ -267,8 +288,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         auto wait_x = [&](int t) {
             ptx::mbar_wait(&full_x[t % K::XS], (uint32_t)((t / K::XS) & 1));
         };
-        // 3xTF32: A' = [hi | hi | lo] (3 DA), B' = [hi | lo] (2 DA): K groups
-        // (A hi, B hi), (A hi, B lo), (A lo, B hi)
+        // 3-product split: A' = [hi | hi | lo] (3 DH), B' = [hi | lo] (2 DH): K groups
+        // (A hi, B hi), (A hi, B lo), (A lo, B hi); one MMA = 32 bytes of K per row
+        // (8 tf32 or 16 fp16), the same core-matrix geometry for both kinds
         auto issue_dist = [&](int t) {
             const int xi = t % K::XS;
             const int b = t % K::NBUF;
@@ -284,12 +306,16 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 const uint32_t xb = ptx::smem_u32(smem + xi * K::XB_BYTES);
                 const uint32_t ap = ptx::smem_u32(smem + K::AP_OFF);
 #pragma unroll
-                for (int ks = 0; ks < 3 * DA / 8; ks++) {
-                    const int g = ks / (DA / 8), kk = ks % (DA / 8);
-                    const int kb = (g == 1 ? DA / 8 : 0) + kk;
+                constexpr int KS = K::DH * K::EB / 32;     // MMAs per product group
+                for (int ks = 0; ks < 3 * KS; ks++) {
+                    const int g = ks / KS, kk = ks % KS;
+                    const int kb = (g == 1 ? KS : 0) + kk;
                     const uint64_t bd = ptx::smem_desc_kmajor(xb + kb * 2 * BK * 16, BK * 16, 128);
                     const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
-                    ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                    if constexpr (K::F16)
+                        ptx::mma_f16_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                    else
+                        ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
                 }
                 ptx::mma_commit(&s_full[b]);
                 ptx::mma_commit(&free_x[xi]);
@@ -346,18 +372,35 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         if (h == 0) {
             // A_i = [2 xs_i, -|xs_i|^2, 1, 0..] split as [hi | hi | lo] (3xTF32), written to
             // shared memory K-major: [3 DA / 4 chunks][128 rows][4 floats]
+            // (F16: fp16 [3 DH / 8 chunks][128 rows][8 halves], entries scaled as in k_prep_tc2)
             const int rl = sub * 32 + lane;
-            float *ap = reinterpret_cast<float *>(smem + K::AP_OFF);
+            if constexpr (K::F16) {
+                uint16_t *ap = reinterpret_cast<uint16_t *>(smem + K::AP_OFF);
 #pragma unroll
-            for (int q = 0; q < DA; q++) {
-                const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
-                const float vh = tf32_rn(v);
-                const float vl = tf32_rn(v - vh);
-                const float parts[3] = {vh, vh, vl};
+                for (int q = 0; q < K::DH; q++) {
+                    const float v = (valid && q < DA) ? kF16Scale * Xa[(r0 + row) * DA + q] : 0.0f;
+                    const __half vh = __float2half_rn(v);
+                    const __half vl = __float2half_rn(v - __half2float(vh));
+                    const __half parts[3] = {vh, vh, vl};
 #pragma unroll
-                for (int pt = 0; pt < 3; pt++) {
-                    const int k = pt * DA + q;
-                    ap[(k >> 2) * (BM * 4) + rl * 4 + (k & 3)] = parts[pt];
+                    for (int pt = 0; pt < 3; pt++) {
+                        const int k = pt * K::DH + q;
+                        ap[(k >> 3) * (BM * 8) + rl * 8 + (k & 7)] = __half_as_ushort(parts[pt]);
+                    }
+                }
+            } else {
+                float *ap = reinterpret_cast<float *>(smem + K::AP_OFF);
+#pragma unroll
+                for (int q = 0; q < DA; q++) {
+                    const float v = valid ? Xa[(r0 + row) * DA + q] : 0.0f;
+                    const float vh = tf32_rn(v);
+                    const float vl = tf32_rn(v - vh);
+                    const float parts[3] = {vh, vh, vl};
+#pragma unroll
+                    for (int pt = 0; pt < 3; pt++) {
+                        const int k = pt * DA + q;
+                        ap[(k >> 2) * (BM * 4) + rl * 4 + (k & 3)] = parts[pt];
+                    }
                 }
             }
             // zero this lane quarter's accumulator columns (the MMAs only add)
@@ -390,9 +433,19 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // t + 1's MUFU work instead of stalling the warp (K1-TC).
         auto quant4 = [&](const uint32_t *sv, int u, uint32_t &a0, uint32_t &a1, uint32_t &a2) {
             uint32_t q[4];
+            uint32_t sw[4] = {sv[4 * u], sv[4 * u + 1], sv[4 * u + 2], sv[4 * u + 3]};
+            if constexpr (K::F16) {   // the MMA gave 2^10 S: rescale, two points per FMUL2
+#pragma unroll
+                for (int v = 0; v < 4; v += 2) {
+                    unsigned long long ps;
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(ps) : "r"(sw[v]), "r"(sw[v + 1]));
+                    asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(ps) : "l"(0x3A8000003A800000ull));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(sw[v]), "=r"(sw[v + 1]) : "l"(ps));
+                }
+            }
 #pragma unroll
             for (int v = 0; v < 4; v++) {
-                const float sj = __uint_as_float(sv[4 * u + v]);
+                const float sj = __uint_as_float(sw[v]);
                 float kv;
                 if (MODE == 2) {
                     // sv holds +rh'^2 with rh' = log2(e) rh (a sum of squares: no clamp);
@@ -554,7 +607,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 // Per point: xs = (x - mean) scale (fp32), e = -|xs|^2.
 //   Xa[i]  = [2 xs_i (d), e_i, 1, 0..]            (DA floats, row operand)
 //   XB tile tt (BK points): B'_j = [xs_j, 1, e_j, 0..] split [hi | lo]
-//   stored K-major for the MMA: [2 DA / 4 chunks][BK rows][4 floats].
+//   stored K-major for the MMA: [2 DA / 4 chunks][BK rows][4 floats] (tf32), or for
+//   DA > 8 (Cfg::F16) times kF16Scale as fp16 [2 DH / 8 chunks][BK rows][8 halves].
 __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad, int d, int DA,
                            const float *__restrict__ scale, const double *__restrict__ mean,
                            float *__restrict__ Xa, float *__restrict__ XB,
@@ -568,6 +622,8 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
             e = fmaf(xs[q], xs[q], e);
         }
         if (j < n) atomicMax(max_sq_bits, __float_as_uint(e));   // e >= 0: bits are ordered
+        const bool f16 = BBMM_TC2_F16DIST && !plain && DA >= BBMM_TC2_F16_MIN_DA;   // Cfg::F16
+        const int DH = f16 ? (DA + 15) & ~15 : DA;
         e = -e;
         const bool ok = j < n;
         for (int q = 0; q < DA; q++) {
@@ -584,16 +640,39 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
                     (ok && q < d) ? xs[q] : 0.0f;
                 continue;
             }
-            const float bh = tf32_rn(b);
-            const float bl = tf32_rn(b - bh);
             const int64_t tt = j / BK;
             const int jj = s_col_of((int)(j - tt * BK));
+            if (f16) {   // fp16 [2 DH / 8 chunks][BK rows][8 halves], times kF16Scale
+                const float bs = kF16Scale * b;
+                const __half bh = __float2half_rn(bs);
+                const __half bl = __float2half_rn(bs - __half2float(bh));
+                uint16_t *tile = reinterpret_cast<uint16_t *>(XB) + tt * (int64_t)(2 * DH * BK);
+                const __half parts[2] = {bh, bl};
+                for (int pt = 0; pt < 2; pt++) {
+                    const int k = pt * DH + q;         // K index in [0, 2 DH)
+                    tile[(k >> 3) * (BK * 8) + jj * 8 + (k & 7)] = __half_as_ushort(parts[pt]);
+                }
+                continue;
+            }
+            const float bh = tf32_rn(b);
+            const float bl = tf32_rn(b - bh);
             float *tile = XB + tt * (int64_t)(2 * DA * BK);
             const float parts[2] = {bh, bl};
             for (int pt = 0; pt < 2; pt++) {
                 const int k = pt * DA + q;             // K index in [0, 2 DA)
                 tile[(k >> 2) * (BK * 4) + jj * 4 + (k & 3)] = parts[pt];
             }
+        }
+        // F16: zero K padding DA..DH-1 of both halves
+        if (f16) {
+            const int64_t tt = j / BK;
+            const int jj = s_col_of((int)(j - tt * BK));
+            uint16_t *tile = reinterpret_cast<uint16_t *>(XB) + tt * (int64_t)(2 * DH * BK);
+            for (int q = DA; q < DH; q++)
+                for (int pt = 0; pt < 2; pt++) {
+                    const int k = pt * DH + q;
+                    tile[(k >> 3) * (BK * 8) + jj * 8 + (k & 7)] = 0;
+                }
         }
     }
 }

@@ -20,6 +20,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
+if os.environ.get("KVAL_LIB"):   # a scratch build (scripts/k1_experiments) instead of the tree's
+    sys.path.insert(0, os.environ["KVAL_LIB"])
 import paper_1809_11165_b200 as bb  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
