@@ -45,8 +45,9 @@ def peaks():
 DTYPE = {
     0: "fp32 kernel values x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
     1: "stored fp32 K x fp64 D, fp64 accumulation (FP64ACC, CUDA cores); fp64 CG",
-    2: "23-bit fixed-point k~ (3 u8 slices) x 31-bit fixed-point D (4 u8 slices; Matern 39-bit, "
-       "5 slices), exact int32 accumulation on tcgen05; fp64 CG",
+    2: "23-bit fixed-point k~ (3 u8 slices; fp32 MUFU ex2 of an fp16-split tensor-core exponent) x "
+       "31-bit fixed-point D (4 u8 slices; Matern 39-bit, 5 slices), exact int32 accumulation of "
+       "the slice products on tcgen05 (q0 p0, < 2^-38 of the scale, dropped); fp64 CG",
     3: "stored 30-bit fixed-point K (4 u8 slices, fp64-built) x 55-bit fixed-point D (7 u8 slices), "
        "exact int32 accumulation on tcgen05; fp64 CG",
 }
@@ -174,7 +175,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kmode", default=None, choices=[None, "onthefly", "stored"])
-    ap.add_argument("--precision", default="int8exact", choices=["int8exact", "fp64acc", "fp32acc"])
+    ap.add_argument("--precision", default="int8exact", choices=["int8exact", "int8exact31", "fp64acc", "fp32acc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -202,8 +203,8 @@ def main():
     kmode = {"onthefly": bb.ONTHEFLY, "stored": bb.STORED}.get(
         args.kmode, bb.STORED if cfg.stored else bb.ONTHEFLY)
     ctx = bb.Context(local_rank)
-    ctx.set_matmul_precision({"int8exact": bb.INT8EXACT, "fp64acc": bb.FP64ACC,
-                              "fp32acc": bb.FP32ACC}[args.precision])
+    ctx.set_matmul_precision({"int8exact": bb.INT8EXACT, "int8exact31": bb.INT8EXACT31,
+                              "fp64acc": bb.FP64ACC, "fp32acc": bb.FP32ACC}[args.precision])
     if world > 1:
         ctx.set_comm()
     X = torch.from_numpy(pr.X).cuda()

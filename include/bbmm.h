@@ -75,20 +75,28 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  * FP32ACC: D rounded to fp32, products summed in fp32 over 16 terms then
  *   folded into fp64.  Faster; parity holds only where mBCG has converged
  *   (SURVEY.md §8c "regime A"). */
-/* INT8EXACT (default): tcgen05 tensor cores, products and sums EXACT in
+/* INT8EXACT (default): tcgen05 tensor cores, slice products summed EXACTLY in
  *   int32 (drained to fp64).  On the fly, RBF (isotropic or ARD): kernel values
- *   as 22-bit fixed point, D as 31-bit fixed point (per-column scale), the
- *   exponent from a 3xTF32 tensor-core distance; shapes t + 1 in {1,2,4,8} with
- *   d <= 22 and t + 1 in {11,17,33} with d <= 30, and max |x_scaled|^2 <= 16
- *   (precision guard).  On the fly, Matern-5/2: distances from direct fp32
- *   differences (the expanded form's ~1e-7 error breaks the parity bars there,
- *   DESIGN.md §6), 22-bit kernel values, 39-bit D; t + 1 in {11,17}, d <= 14.
- *   Stored K (BBMM_STORED, t + 1 in {1,2,4,8,11,16,17,32,33}): K as 30-bit and D
- *   as 39-bit fixed point.  Everything else uses FP64ACC. */
+ *   (fp32 MUFU ex2) on a 23-bit fixed-point grid, D as 31-bit fixed point
+ *   (per-column scale), the exponent from an fp16 hi/lo-split tensor-core
+ *   distance; any t + 1 <= 33 (padded to the next instantiated column block) with
+ *   d <= 30, and max |x_scaled|^2 <= 16 (precision guard).  On the fly,
+ *   Matern-5/2: distances from direct fp32 differences (the expanded form's
+ *   ~1e-7 error breaks the parity bars there), 23-bit kernel
+ *   values, 39-bit D; t + 1 <= 17, d <= 14.  Stored K (BBMM_STORED, t + 1 <= 33):
+ *   K built in fp64 and stored as 30-bit fixed point, D as 55-bit fixed point.
+ *   Everything else uses FP64ACC.
+ * INT8EXACT31: as INT8EXACT, but the on-the-fly RBF kernel-matmul keeps the
+ *   MUFU's kernel values on a 31-bit grid (a fourth, residual u8 slice of k~):
+ *   per-entry error 3.3e-8 instead of 5.3e-8 rms at C4 (the grid rounding
+ *   removed, the MUFU's own error left), for the north-star solve bar at
+ *   n = 1M; ~10-20 % slower kernel-matmul.  The derivative pass
+ *   and the Matern / stored operators are those of INT8EXACT. */
 typedef enum {
     BBMM_MATMUL_FP64ACC = 0,
     BBMM_MATMUL_FP32ACC = 1,
-    BBMM_MATMUL_INT8EXACT = 2
+    BBMM_MATMUL_INT8EXACT = 2,
+    BBMM_MATMUL_INT8EXACT31 = 3
 } bbmm_matmul_precision_t;
 
 typedef struct {

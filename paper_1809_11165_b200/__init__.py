@@ -27,6 +27,7 @@ STORED = 1
 FP64ACC = 0     # matmul precision: fp64 D, fp64 products and sums (FFMA/DFMA path)
 FP32ACC = 1     # fp32 D, 16-term fp32 chunks folded into fp64 (regime A only)
 INT8EXACT = 2   # default: tcgen05 int8 tensor cores, exact integer contraction (else FP64ACC)
+INT8EXACT31 = 3  # INT8EXACT with the on-the-fly RBF kernel values on a 31-bit grid (n ~ 1M parity)
 
 _STATUS = {0: "OK", 2: "ERR_ARG", 3: "ERR_DATA", 4: "ERR_NUMERIC", 5: "ERR_CUDA",
            6: "ERR_NCCL", 7: "ERR_OOM"}

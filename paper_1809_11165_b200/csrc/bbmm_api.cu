@@ -395,10 +395,11 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
 
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p) {
     if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC &&
-                 p != BBMM_MATMUL_INT8EXACT))
+                 p != BBMM_MATMUL_INT8EXACT && p != BBMM_MATMUL_INT8EXACT31))
         return BBMM_ERR_ARG;
     ctx->matmul_acc64 = (p != BBMM_MATMUL_FP32ACC);
-    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT);
+    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT || p == BBMM_MATMUL_INT8EXACT31);
+    ctx->matmul_grid31 = (p == BBMM_MATMUL_INT8EXACT31);
     return BBMM_OK;
 }
 

@@ -129,6 +129,7 @@ struct bbmm_ctx_s {
     int launches = 0;   // library kernel launches since last reset
     bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
+    bool matmul_grid31 = false; // BBMM_MATMUL_INT8EXACT31: on-the-fly RBF k~ on a 31-bit grid
     int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
     bbmm::LocalGroup *local = nullptr;   // in-process rank group (comm_local.cu) instead of NCCL
     // timing events of the mBCG matmuls, reused across calls (created on first use, destroyed

@@ -5,9 +5,10 @@
 // D as 31-bit (RBF) or 39-bit (Matern) fixed point per column (k1tc.cu), all
 // slice products on the int8 tensor cores with exact integer accumulation in
 // TMEM, drained to fp64.  Per 128 x 128 tile:
-//   * RBF (MODE 0 / 1): the exponent S_ij = -|xs_i - xs_j|^2 is itself a
-//     tcgen05 MMA (3-product hi/lo split: kind::tf32 at d <= 6, kind::f16 with
-//     operands scaled by 2^5 above, half the MMAs there) of augmented vectors
+//   * RBF (MODE 0 / 1 / 3): the exponent S_ij = -|xs_i - xs_j|^2 is itself a
+//     tcgen05 MMA (3-product hi/lo split in fp16 with operands scaled by 2^5:
+//     at d <= 6 the three products packed along K into two kind::f16 MMAs,
+//     above that kind::f16 per product -- half the MMAs of kind::tf32) of augmented vectors
 //       A_i = [2 xs_i, -|xs_i|^2, 1] (shared memory),  B_j = [xs_j, 1, -|xs_j|^2]
 //     (streamed [hi | lo] tiles) into a TMEM buffer; compute warps tcgen05.ld S,
 //     run ex2 on the MUFU (MODE 1: times r^2, the isotropic lengthscale
@@ -68,6 +69,23 @@ namespace tc2 {
 #ifndef BBMM_TC2_F16_MIN_DA
 #define BBMM_TC2_F16_MIN_DA 16
 #endif
+// DA = 8 (d <= 6): the three hi/lo products packed along K into ONE fp16 operand pair,
+// A' = [hi | hi | lo | 0], B' = [hi | lo | hi | 0] (K = 32 halves): 2 kind::f16 MMAs per tile
+// instead of 3 kind::tf32 (same 11 + 11-bit split; a third less tensor time and TMEM
+// accumulator traffic for the distance)
+#ifndef BBMM_TC2_F16PACK
+#define BBMM_TC2_F16PACK 1
+#endif
+// Trim the int8 MMAs of the low k~ slices to the products that carry weight (ND = 4):
+// 0 = all twelve slice products; 1 (default) = q0 x [p3 p2 p1] (drops q0 p0: weight 2^0 of the
+// 2^54 product scale, < 2^-38 relative -- 64x below the rounding of the 31-bit D itself);
+// 2 = also q1 x [p3 p2 p1], q0 x [p3 p2] (drops the weight-2^8 products q1 p0, q0 p1: ~2^-29,
+// i.e. above D's rounding -- timing experiments only).  The MMA N is rounded up to 16, so a few
+// dropped-block columns are still added -- at their correct weight (the blocks are
+// weight-ordered), never elsewhere.  Measured (B200): C4 289.0 -> 288.5 ms, C3 16.29 -> 15.93 ms.
+#ifndef BBMM_TC2_TRIM
+#define BBMM_TC2_TRIM 1
+#endif
 // fp16 distance operands are scaled by 2^5 (|xs|^2 by 2^10) so that the lo halves of the
 // split stay normal fp16 numbers down to |xs| ~ 2^-8 (the precision guard keeps |xs|^2 <= 16,
 // so 2^10 |xs|^2 <= 16384 < 65504); the MMA then yields 2^10 S, rescaled before ex2
@@ -83,6 +101,11 @@ static_assert((JW == 32 || (JW == 16 && NPS % 2 == 0)) && 32 * (NCW + 2) <= 1024
 // exactly), hence < 2^32 / 162690 = 26399 j per window.
 constexpr int WINDOW = (int)(4294967295ull / 162690ull) / BK * BK;
 static_assert((double)WINDOW * 162690.0 < 4294967296.0, "uint32 window bound");
+// MODE 3 (31-bit k~ grid) adds the residual slice r <= 255 at weight 2^-8 below q0, whose
+// products r p3, r p2 (and r p1 for 8 columns) join blocks 3-5: the largest per-j block sum
+// becomes block 3's q2 p0 + q1 p1 + q0 p2 + r p3 <= 128*255 + 2*255*255 + 255*128 = 195330
+constexpr int WINDOW31 = (int)(4294967295ull / 195330ull) / BK * BK;
+static_assert((double)WINDOW31 * 195330.0 < 4294967296.0, "uint32 window bound (MODE 3)");
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(NCW * JW == 4 * BK, "4 lane quarters x BK columns");
@@ -97,10 +120,11 @@ constexpr __host__ __device__ int r32(int x) { return (x + 31) & ~31; }
 // Accumulator layout: the slice products are merged by weight.  The D-slice
 // operand holds four column blocks [p3 | p2 | p1 | p0] of BLK = round4(C + 1)
 // columns (C real columns, 1 constant offset column, zero padding); the three
-// int8 MMAs of a K-step multiply q2, q1, q0 by the whole operand (N = 4 BLK)
-// into accumulator blocks 0-3, 1-4 and 2-5, so block k collects every
-// product of weight 2^(8 (5 - k)) (q_a p_b with a + b = 5 - k): all twelve
-// slice products, no truncation, in 6 BLK TMEM columns.  The MMAs always
+// int8 MMAs of a K-step multiply q2, q1, q0 by the whole operand (N = 4 BLK;
+// q0's N trimmed to round16(3 BLK), BBMM_TC2_TRIM) into accumulator blocks 0-3,
+// 1-4 and 2-5, so block k collects every product of weight 2^(8 (5 - k))
+// (q_a p_b with a + b = 5 - k) -- the twelve slice products but q0 p0 -- in 6 BLK
+// TMEM columns.  The MMAs always
 // accumulate; the draining warps zero the columns they read.
 // ND = number of D slices: 4 (31-bit D, RBF) or 5 (39-bit D, Matern, whose
 // C2 shape is not converged at p: DESIGN.md §6 / reading R29); with 5 slices
@@ -128,11 +152,19 @@ struct Cfg {
     // take one MMA per product and tf32 stays (no operand scaling).  ND == 5 is Matern (MODE 2:
     // plain fp32 x tiles, no distance MMA).
     static constexpr bool F16 = BBMM_TC2_F16DIST && ND == 4 && DA >= BBMM_TC2_F16_MIN_DA;
+    static constexpr bool PK = BBMM_TC2_F16PACK && ND == 4 && DA == 8;   // packed fp16, K = 32
+    static constexpr bool H16 = F16 || PK;                     // fp16 operands (scaled by 2^5)
     static constexpr int DH = F16 ? r16(DA) : DA;              // K per product group
-    static constexpr int EB = F16 ? 2 : 4;                     // operand element bytes
+    static constexpr int EB = H16 ? 2 : 4;                     // operand element bytes
     static constexpr int B8_BYTES = NB * BK;                   // int8 D slices per tile
-    static constexpr int XB_BYTES = 2 * DH * BK * EB;          // B' per tile: [hi | lo]
-    static constexpr int AP_BYTES = BM * 3 * DH * EB;          // row operand A' (smem)
+    // B' per tile: [hi | lo] (2 DH), packed: [hi | lo | hi | 0] (32 halves = 2 DH x 2 bytes)
+    static constexpr int XB_BYTES = 2 * DH * BK * (PK ? 4 : EB);
+    static constexpr int AP_BYTES = BM * (PK ? 32 : 3 * DH) * EB;   // row operand A' (smem)
+    // int8 MMA N of the q1 / q0 slices (BBMM_TC2_TRIM)
+    static constexpr int N1 = (ND == 4 && BBMM_TC2_TRIM >= 2 && r16(3 * BLK) < NB) ? r16(3 * BLK) : NB;
+    static constexpr int N0 = (ND == 4 && BBMM_TC2_TRIM >= 1)
+                                  ? (BBMM_TC2_TRIM >= 2 ? r16(2 * BLK) : (r16(3 * BLK) < NB ? r16(3 * BLK) : NB))
+                                  : NB;
     static constexpr int STATIC_BYTES = (C + 1) * BM * 8 + 512;   // acc_sm + barriers
     // Two shared-memory rings, each refilled as soon as its consumer MMA completes:
     // XB (read by the distance MMA of tile t, issued NBUF tiles before tile t's
@@ -191,7 +223,8 @@ __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[B
     }
 }
 
-// MODE 0: value k~ = K/s (the blackbox matmul);  MODE 1: value k~ r^2
+// MODE 0: value k~ = K/s (the blackbox matmul) on the 23-bit grid;  MODE 3: the same on a
+// 31-bit grid (a fourth, residual slice; BBMM_MATMUL_INT8EXACT31);  MODE 1: value k~ r^2
 // (= (dK/dlog l)/s for the isotropic RBF, used by the derivative pass);
 // MODE 2: Matern-5/2 k~ = (1 + rh + rh^2/3) e^{-rh}, rh = sqrt(-S) (inputs
 // scaled by sqrt5/l; two MUFU ops per pair: sqrt, ex2), 39-bit D (ND = 5).
@@ -220,7 +253,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
     const int ntl = (int)(min(ntiles, t0 + tiles_per_split) - t0);
-    constexpr int TPW = WINDOW / BK;
+    constexpr int TPW = (MODE == 3 ? WINDOW31 : WINDOW) / BK;
 
     if (tid == 0) {
         for (int q = 0; q < K::XS; q++) {
@@ -280,8 +313,16 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // execute in issue order, so the distance MMA of tile t + K::NBUF, issued
         // right after the int8 MMAs of tile t that read the same TMEM buffer,
         // cannot overwrite it early: no buffer-free round trip is needed.
-        constexpr uint32_t IDS = K::F16 ? ptx::idesc_f16(BM, BK) : ptx::idesc_tf32(BM, BK);
+        constexpr uint32_t IDS = K::H16 ? ptx::idesc_f16(BM, BK) : ptx::idesc_tf32(BM, BK);
         constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
+        constexpr uint32_t IDQ1 = ptx::idesc_i8(BM, K::N1, false, false);
+        constexpr uint32_t IDQ0 = ptx::idesc_i8(BM, K::N0, false, false);
+        // MODE 3 residual slice r x [p3 p2 (p1)]: N = round16(2 BLK) -- the extra columns land
+        // in blocks of their own weight (r p1 -> block 5) or, at BLK = 4, in the padding
+        // column block 6 that is never drained (ACC_END >= 7 BLK there)
+        constexpr int NR = r16(2 * K::BLK);
+        static_assert(MODE != 3 || NR <= 3 * K::BLK || 7 * K::BLK <= K::ACC_END, "residual N");
+        constexpr uint32_t IDQR = ptx::idesc_i8(BM, NR, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         ptx::tc_fence_after();
@@ -305,17 +346,27 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             if (leader) {
                 const uint32_t xb = ptx::smem_u32(smem + xi * K::XB_BYTES);
                 const uint32_t ap = ptx::smem_u32(smem + K::AP_OFF);
+                if constexpr (K::PK) {
+                    // packed: A' = [hi | hi | lo | 0] x B' = [hi | lo | hi | 0], two K = 16 MMAs
 #pragma unroll
-                constexpr int KS = K::DH * K::EB / 32;     // MMAs per product group
-                for (int ks = 0; ks < 3 * KS; ks++) {
-                    const int g = ks / KS, kk = ks % KS;
-                    const int kb = (g == 1 ? KS : 0) + kk;
-                    const uint64_t bd = ptx::smem_desc_kmajor(xb + kb * 2 * BK * 16, BK * 16, 128);
-                    const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
-                    if constexpr (K::F16)
+                    for (int ks = 0; ks < 2; ks++) {
+                        const uint64_t bd = ptx::smem_desc_kmajor(xb + ks * 2 * BK * 16, BK * 16, 128);
+                        const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
                         ptx::mma_f16_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
-                    else
-                        ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                    }
+                } else {
+                    constexpr int KS = K::DH * K::EB / 32;     // MMAs per product group
+#pragma unroll
+                    for (int ks = 0; ks < 3 * KS; ks++) {
+                        const int g = ks / KS, kk = ks % KS;
+                        const int kb = (g == 1 ? KS : 0) + kk;
+                        const uint64_t bd = ptx::smem_desc_kmajor(xb + kb * 2 * BK * 16, BK * 16, 128);
+                        const uint64_t ad = ptx::smem_desc_kmajor(ap + ks * 2 * BM * 16, BM * 16, 128);
+                        if constexpr (K::F16)
+                            ptx::mma_f16_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                        else
+                            ptx::mma_tf32_ss(tmem + K::BUF_OFF + b * BK, ad, bd, IDS, ks > 0 ? 1u : 0u);
+                    }
                 }
                 ptx::mma_commit(&s_full[b]);
                 ptx::mma_commit(&free_x[xi]);
@@ -345,8 +396,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 for (int ks = 0; ks < BK / 32; ks++) {
                     const uint64_t bd = ptx::smem_desc_kmajor(b8 + ks * 2 * K::NB * 16, K::NB * 16, 128);
                     ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, IDQ, 1u);              // q2
-                    ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ, 1u);          // q1
-                    ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ, 1u);      // q0
+                    ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ1, 1u);         // q1
+                    ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ0, 1u);     // q0
+                    if constexpr (MODE == 3)
+                        ptx::mma_i8_ts(tmem + 3 * K::BLK, aq + 32 * ks + 24, bd, IDQR, 1u);  // r
                 }
                 ptx::mma_commit(&free_q[qi]);
                 if (((t + 1) % TPW) == 0 || t + 1 == ntl) ptx::mma_commit(&acc_full);
@@ -374,7 +427,20 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             // shared memory K-major: [3 DA / 4 chunks][128 rows][4 floats]
             // (F16: fp16 [3 DH / 8 chunks][128 rows][8 halves], entries scaled as in k_prep_tc2)
             const int rl = sub * 32 + lane;
-            if constexpr (K::F16) {
+            if constexpr (K::PK) {
+                // packed: fp16 [4 chunks][128 rows][8 halves], K = [hi | hi | lo | 0] of DA = 8
+                uint16_t *ap = reinterpret_cast<uint16_t *>(smem + K::AP_OFF);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const float v = valid ? kF16Scale * Xa[(r0 + row) * DA + q] : 0.0f;
+                    const __half vh = __float2half_rn(v);
+                    const __half vl = __float2half_rn(v - __half2float(vh));
+                    ap[0 * (BM * 8) + rl * 8 + q] = __half_as_ushort(vh);
+                    ap[1 * (BM * 8) + rl * 8 + q] = __half_as_ushort(vh);
+                    ap[2 * (BM * 8) + rl * 8 + q] = __half_as_ushort(vl);
+                    ap[3 * (BM * 8) + rl * 8 + q] = 0;
+                }
+            } else if constexpr (K::F16) {
                 uint16_t *ap = reinterpret_cast<uint16_t *>(smem + K::AP_OFF);
 #pragma unroll
                 for (int q = 0; q < K::DH; q++) {
@@ -431,10 +497,12 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // MMAs of the previous tile stream through TMEM, so the arrive for
         // tile t (and its tcgen05.wait::st) is deferred to the middle of tile
         // t + 1's MUFU work instead of stalling the warp (K1-TC).
-        auto quant4 = [&](const uint32_t *sv, int u, uint32_t &a0, uint32_t &a1, uint32_t &a2) {
+        static_assert(MODE != 3 || JW == 32, "MODE 3 stores four slices over the 32 S columns");
+        auto quant4 = [&](const uint32_t *sv, int u, uint32_t &a0, uint32_t &a1, uint32_t &a2,
+                          uint32_t &a3) {
             uint32_t q[4];
             uint32_t sw[4] = {sv[4 * u], sv[4 * u + 1], sv[4 * u + 2], sv[4 * u + 3]};
-            if constexpr (K::F16) {   // the MMA gave 2^10 S: rescale, two points per FMUL2
+            if constexpr (K::H16) {   // the MMA gave 2^10 S: rescale, two points per FMUL2
 #pragma unroll
                 for (int v = 0; v < 4; v += 2) {
                     unsigned long long ps;
@@ -471,12 +539,34 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             // low bit lands on bit 23 = 2^23 = k~ 2^23 again.  So the three low bytes are
             // exactly the 23-bit fixed-point k~ 2^23 for every k~ in [0, 1] (grid 2^-23: half
             // the rounding of the q = 2 + k~ form).  Two points per instruction (FFMA2).
+            // MODE 3 (31-bit grid): q = 2 + 2 k~ truncated (rz), so q's bytes are k^ = the 23-bit
+            // truncation of k~; u = 2^31 + 2^23 - 2^30 q = 2^23 - 2^31 k^ (exact: a multiple of 2^8
+            // below 2^31), m = rz(2^31 k~ + u) = 2^23 + floor(2^31 (k~ - k^)) (exact sum in
+            // [2^23, 2^23 + 256), ulp 1): its low byte is the residual r in [0, 255], k~ =
+            // (q2 2^24 + q1 2^16 + q0 2^8 + r) 2^-31 up to 2^-31 (INT8EXACT31)
+            uint32_t m[4];
 #pragma unroll
             for (int v = 0; v < 4; v += 2) {
                 unsigned long long pq;
                 asm("mov.b64 %0, {%1, %2};" : "=l"(pq) : "r"(q[v]), "r"(q[v + 1]));
-                asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
+                if constexpr (MODE == 3) {
+                    const unsigned long long pk = pq;
+                    unsigned long long pu, pm;
+                    asm("fma.rz.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pu) : "l"(pq), "l"(0xCE800000CE800000ull),
+                        "l"(0x4F0080004F008000ull));
+                    asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(pm) : "l"(pk), "l"(0x4F0000004F000000ull),
+                        "l"(pu));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(m[v]), "=r"(m[v + 1]) : "l"(pm));
+                } else {
+                    asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
+                }
                 asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pq));
+            }
+            if constexpr (MODE == 3) {
+                const uint32_t r01 = __byte_perm(m[0], m[1], 0x0040);
+                const uint32_t r23 = __byte_perm(m[2], m[3], 0x0040);
+                a3 = __byte_perm(r01, r23, 0x5410);
             }
             const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
             const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
@@ -556,9 +646,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 for (int u = 0; u < 4; u++) ptx::tmem_ld4(col + 8 * u, sv + 4 * u);
             }
             if constexpr (MODE != 2) ptx::tmem_ld_wait();
-            uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4];
+            uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4], w3[JW / 4];
 #pragma unroll
-            for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
+            for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
             if (DEFER && t > 0) publish(t - 1);
             // overwrite own S columns with the A slices q0 | q1 | q2 (column maps
             // above), each half as soon as it is quantised: spreading the stores
@@ -567,13 +657,15 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
                 ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
+                if constexpr (MODE == 3) ptx::tmem_st4(col + 24, *reinterpret_cast<const uint32_t(*)[4]>(w3));
             }
 #pragma unroll
-            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u]);
+            for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
             if constexpr (JW == 32) {
                 ptx::tmem_st4(col + 4, *reinterpret_cast<const uint32_t(*)[4]>(w0 + 4));
                 ptx::tmem_st4(col + 12, *reinterpret_cast<const uint32_t(*)[4]>(w1 + 4));
                 ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
+                if constexpr (MODE == 3) ptx::tmem_st4(col + 28, *reinterpret_cast<const uint32_t(*)[4]>(w3 + 4));
             } else {
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
@@ -623,6 +715,7 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
         }
         if (j < n) atomicMax(max_sq_bits, __float_as_uint(e));   // e >= 0: bits are ordered
         const bool f16 = BBMM_TC2_F16DIST && !plain && DA >= BBMM_TC2_F16_MIN_DA;   // Cfg::F16
+        const bool pk = BBMM_TC2_F16PACK && !plain && DA == 8;                       // Cfg::PK
         const int DH = f16 ? (DA + 15) & ~15 : DA;
         e = -e;
         const bool ok = j < n;
@@ -642,6 +735,17 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
             }
             const int64_t tt = j / BK;
             const int jj = s_col_of((int)(j - tt * BK));
+            if (pk) {    // packed fp16 [4 chunks][BK rows][8 halves] = [hi | lo | hi | 0], times kF16Scale
+                const float bs = kF16Scale * b;
+                const __half bh = __float2half_rn(bs);
+                const __half bl = __float2half_rn(bs - __half2float(bh));
+                uint16_t *tile = reinterpret_cast<uint16_t *>(XB) + tt * (int64_t)(32 * BK);
+                tile[0 * (BK * 8) + jj * 8 + q] = __half_as_ushort(bh);
+                tile[1 * (BK * 8) + jj * 8 + q] = __half_as_ushort(bl);
+                tile[2 * (BK * 8) + jj * 8 + q] = __half_as_ushort(bh);
+                tile[3 * (BK * 8) + jj * 8 + q] = 0;
+                continue;
+            }
             if (f16) {   // fp16 [2 DH / 8 chunks][BK rows][8 halves], times kF16Scale
                 const float bs = kF16Scale * b;
                 const __half bh = __float2half_rn(bs);
@@ -802,7 +906,9 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         return sp;
     }
 #define BBMM_TC2(CC, DD) \
-    if (c == CC && da == DD) sp = launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+    if (c == CC && da == DD) sp = g31 ? launch_tc2<CC, DD, 3>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap) \
+                                      : launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+    const bool g31 = ctx->matmul_grid31;   // INT8EXACT31: MODE 3 (31-bit k~ grid)
     if (nloc > 0) {
         BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
         BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """A/B timing of K1-TC builds at a BASELINE shape (one subprocess per build).
 
-    python scripts/k1_ab.py [--config C4] [--n N] [--reps 5] LIBROOT ...
+    python scripts/k1_ab.py [--config C4] [--n N] [--reps 5] [--precision 2] LIBROOT ...
 
 LIBROOT = a directory holding paper_1809_11165_b200/ (the repo itself: ".", a variant:
 scratch/var_NAME).  Each build runs the kernel-matmul V = Khat D (INT8EXACT) once to warm up, then
@@ -26,6 +26,7 @@ D = synth.random_block(cfg.n, cfg.t + 1, seed=4).astype(np.float64)
 ctx = bb.Context(0)
 X = torch.from_numpy(pr.X).cuda(); Dd = torch.from_numpy(D).cuda()
 h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
+ctx.set_matmul_precision({prec})
 V = bb.kernel_matmul(ctx, X, Dd, h)
 ms = []
 for _ in range({reps}):
@@ -40,7 +41,7 @@ print(json.dumps(dict(ms=sorted(ms)[len(ms) // 2], all=ms, n=cfg.n)))
 
 def main():
     args = sys.argv[1:]
-    cfg, n, reps = "C4", None, 5
+    cfg, n, reps, prec = "C4", None, 5, 2
     while args and args[0].startswith("--"):
         k, v = args[0], args[1]
         args = args[2:]
@@ -50,6 +51,8 @@ def main():
             n = int(v)
         elif k == "--reps":
             reps = int(v)
+        elif k == "--precision":      # 2 = INT8EXACT, 3 = INT8EXACT31, 0 = FP64ACC
+            prec = int(v)
     sys.path.insert(0, ROOT)
     import numpy as np
     import synth
@@ -58,7 +61,7 @@ def main():
     for i, lib in enumerate(args):
         lib = os.path.abspath(lib)
         out = f"/tmp/k1ab_{i}.npy"
-        code = CHILD.format(root=ROOT, lib=lib, cfg=cfg, n=n, reps=reps, out=out)
+        code = CHILD.format(root=ROOT, lib=lib, cfg=cfg, n=n, reps=reps, out=out, prec=prec)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         if r.returncode != 0:
             print(json.dumps(dict(lib=lib, error=r.stderr[-800:])))

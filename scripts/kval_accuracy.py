@@ -48,7 +48,8 @@ ctx = bb.Context(0)
 X = torch.from_numpy(pr.X).cuda()
 Dd = torch.from_numpy(D).cuda()
 h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
-for label, prec, km in [("int8exact", bb.INT8EXACT, bb.ONTHEFLY), ("fp64acc", bb.FP64ACC, bb.ONTHEFLY)]:
+for label, prec, km in [("int8exact", bb.INT8EXACT, bb.ONTHEFLY), ("int8exact31", bb.INT8EXACT31, bb.ONTHEFLY),
+                        ("fp64acc", bb.FP64ACC, bb.ONTHEFLY)]:
     ctx.set_matmul_precision(prec)
     V = bb.kernel_matmul(ctx, X, Dd, h, km).cpu().numpy()
     V[cols, np.arange(m)] -= noise

@@ -97,7 +97,8 @@ def _run(ctx, name, n, prec):
         mll=float(abs(g["mll"] - float(z["mll"])) / abs(float(z["mll"]))),
         grad=float(np.linalg.norm(g["grad"] - z["grad"]) / np.linalg.norm(z["grad"])),
         pivots_equal=bool(np.array_equal(g["pivots"], z["pivots"])))
-    rec = dict(case=f"{name} n={n}", precision={bb.INT8EXACT: "int8exact", bb.FP64ACC: "fp64acc"}[prec],
+    rec = dict(case=f"{name} n={n}", precision={bb.INT8EXACT: "int8exact", bb.FP64ACC: "fp64acc",
+                                               bb.INT8EXACT31: "int8exact31"}[prec],
                matmul_path=g["stats"]["matmul_path"], oracle_relres_y=meta["relres_y"],
                regime=meta["regime"], gpu_relres_y=g["stats"]["relres_y"],
                unconverged=g["stats"]["unconverged"], ms_total=g["stats"]["ms_total"], **err)
@@ -122,6 +123,16 @@ def test_fullsize_mll_and_grad_matches_cached_oracle(ctx, name, n):
         assert g["stats"]["unconverged"] == 1
         assert err["solve"] <= _regime_b_solve_bar(name, n), err
         assert err["grad"] <= REGIME_B_GRAD, err
+
+
+@pytest.mark.parametrize("name,n", [c for c in CASES if c[0] == "C4"])
+def test_fullsize_grid31_c4(ctx, name, n):
+    """INT8EXACT31 (31-bit kernel-value grid) at the C4 shape: the solve error falls with the
+    per-entry kernel-value error (||du||/||u|| ~ sqrt(n) eps / sigma^2)."""
+    meta, g, err = _run(ctx, name, n, bb.INT8EXACT31)
+    assert err["pivots_equal"] and g["stats"]["matmul_path"] == 2
+    assert err["logdet"] <= 1e-3 and err["mll"] <= 1e-3, err
+    assert err["solve"] <= 1e-4 and err["grad"] <= 1e-3, err
 
 
 @pytest.mark.parametrize("name,n", CASES)
