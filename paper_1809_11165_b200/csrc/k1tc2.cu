@@ -83,6 +83,11 @@ namespace tc2 {
 // i.e. above D's rounding -- timing experiments only).  The MMA N is rounded up to 16, so a few
 // dropped-block columns are still added -- at their correct weight (the blocks are
 // weight-ordered), never elsewhere.  Measured (B200): C4 289.0 -> 288.5 ms, C3 16.29 -> 15.93 ms.
+// timing ablations of MODE 3 (results wrong by construction): 1 = no residual MMA,
+// 2 = no residual TMEM stores, 3 = no residual arithmetic (zero slice)
+#ifndef BBMM_TC2_ABL
+#define BBMM_TC2_ABL 0
+#endif
 #ifndef BBMM_TC2_TRIM
 #define BBMM_TC2_TRIM 1
 #endif
@@ -398,7 +403,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, IDQ, 1u);              // q2
                     ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ1, 1u);         // q1
                     ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ0, 1u);     // q0
-                    if constexpr (MODE == 3)
+                    if constexpr (MODE == 3 && BBMM_TC2_ABL != 1)
                         ptx::mma_i8_ts(tmem + 3 * K::BLK, aq + 32 * ks + 24, bd, IDQR, 1u);  // r
                 }
                 ptx::mma_commit(&free_q[qi]);
@@ -534,39 +539,51 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 if (MODE == 1) kv *= fmaxf(-sj, 0.0f);
                 q[v] = __float_as_uint(kv);
             }
+            if constexpr (MODE == 3 && BBMM_TC2_ABL != 3) {
+                // 31-bit grid: the fixed-point value F = k~ 2^31 (exact for k~ >= 2^-8, where the
+                // fp32 k~ has no bits below 2^-31; floor below) as two 16-bit halves, F = H 2^16 + L:
+                //   h = rz(2^15 k~ + 2^23)              = 2^23 + H,  H = floor(2^15 k~) <= 2^15
+                //   u = 2^39 + 2^23 - 2^16 h             = 2^23 - 2^16 H (exact: a multiple of 2^16)
+                //   m = rz(2^31 k~ + u)                  = 2^23 + L,  L = floor(2^31 k~ - 2^16 H) < 2^16
+                // (each FMA's exact result is representable or truncated at ulp 1); the low two
+                // bytes of h and m are the four u8 slices, k~ = (H.b1 2^24 + H.b0 2^16 + L.b1 2^8 +
+                // L.b0) 2^-31 -- the weights of INT8EXACT's q2 q1 q0 plus the residual slot below q0,
+                // 8 byte permutes per 4 pairs (INT8EXACT31)
+                uint32_t hw[4], mw[4];
+#pragma unroll
+                for (int v = 0; v < 4; v += 2) {
+                    unsigned long long pk, ph, pu, pm;
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(pk) : "r"(q[v]), "r"(q[v + 1]));
+                    asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(ph) : "l"(pk), "l"(0x4700000047000000ull),
+                        "l"(0x4B0000004B000000ull));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pu) : "l"(ph), "l"(0xC7800000C7800000ull),
+                        "l"(0x5300008053000080ull));
+                    asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(pm) : "l"(pk), "l"(0x4F0000004F000000ull),
+                        "l"(pu));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(hw[v]), "=r"(hw[v + 1]) : "l"(ph));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(mw[v]), "=r"(mw[v + 1]) : "l"(pm));
+                }
+                const uint32_t t01 = __byte_perm(hw[0], hw[1], 0x5140);
+                const uint32_t t23 = __byte_perm(hw[2], hw[3], 0x5140);
+                const uint32_t l01 = __byte_perm(mw[0], mw[1], 0x5140);
+                const uint32_t l23 = __byte_perm(mw[2], mw[3], 0x5140);
+                a2 = __byte_perm(t01, t23, 0x7632);      // H.b1: weight 2^24 (q2's)
+                a1 = __byte_perm(t01, t23, 0x5410);      // H.b0: 2^16 (q1's)
+                a0 = __byte_perm(l01, l23, 0x7632);      // L.b1: 2^8  (q0's)
+                a3 = __byte_perm(l01, l23, 0x5410);      // L.b0: 2^0  (residual slot)
+                return;
+            }
             // q = 2 + 2 k~ in [2, 4]: for k~ < 1 the exponent is 128 (bit 23 = 0) and the
             // mantissa is k~ 2^23 rounded to nearest; k~ = 1 gives 4.0 = exponent 129, whose
             // low bit lands on bit 23 = 2^23 = k~ 2^23 again.  So the three low bytes are
             // exactly the 23-bit fixed-point k~ 2^23 for every k~ in [0, 1] (grid 2^-23: half
             // the rounding of the q = 2 + k~ form).  Two points per instruction (FFMA2).
-            // MODE 3 (31-bit grid): q = 2 + 2 k~ truncated (rz), so q's bytes are k^ = the 23-bit
-            // truncation of k~; u = 2^31 + 2^23 - 2^30 q = 2^23 - 2^31 k^ (exact: a multiple of 2^8
-            // below 2^31), m = rz(2^31 k~ + u) = 2^23 + floor(2^31 (k~ - k^)) (exact sum in
-            // [2^23, 2^23 + 256), ulp 1): its low byte is the residual r in [0, 255], k~ =
-            // (q2 2^24 + q1 2^16 + q0 2^8 + r) 2^-31 up to 2^-31 (INT8EXACT31)
-            uint32_t m[4];
 #pragma unroll
             for (int v = 0; v < 4; v += 2) {
                 unsigned long long pq;
                 asm("mov.b64 %0, {%1, %2};" : "=l"(pq) : "r"(q[v]), "r"(q[v + 1]));
-                if constexpr (MODE == 3) {
-                    const unsigned long long pk = pq;
-                    unsigned long long pu, pm;
-                    asm("fma.rz.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
-                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pu) : "l"(pq), "l"(0xCE800000CE800000ull),
-                        "l"(0x4F0080004F008000ull));
-                    asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(pm) : "l"(pk), "l"(0x4F0000004F000000ull),
-                        "l"(pu));
-                    asm("mov.b64 {%0, %1}, %2;" : "=r"(m[v]), "=r"(m[v + 1]) : "l"(pm));
-                } else {
-                    asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
-                }
+                asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
                 asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pq));
-            }
-            if constexpr (MODE == 3) {
-                const uint32_t r01 = __byte_perm(m[0], m[1], 0x0040);
-                const uint32_t r23 = __byte_perm(m[2], m[3], 0x0040);
-                a3 = __byte_perm(r01, r23, 0x5410);
             }
             const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
             const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
@@ -575,6 +592,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             a0 = __byte_perm(t01, t23, 0x5410);
             a2 = __byte_perm(t01, t23, 0x7632);
             a1 = __byte_perm(u01, u23, 0x5410);
+            a3 = 0u;
         };
         // publish tile tp's A slices (stores issued earlier), then drain the
         // accumulators if tp closed a window
@@ -657,7 +675,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
                 ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
-                if constexpr (MODE == 3) ptx::tmem_st4(col + 24, *reinterpret_cast<const uint32_t(*)[4]>(w3));
+                if constexpr (MODE == 3 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 24, *reinterpret_cast<const uint32_t(*)[4]>(w3));
             }
 #pragma unroll
             for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
@@ -665,7 +683,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 ptx::tmem_st4(col + 4, *reinterpret_cast<const uint32_t(*)[4]>(w0 + 4));
                 ptx::tmem_st4(col + 12, *reinterpret_cast<const uint32_t(*)[4]>(w1 + 4));
                 ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
-                if constexpr (MODE == 3) ptx::tmem_st4(col + 28, *reinterpret_cast<const uint32_t(*)[4]>(w3 + 4));
+                if constexpr (MODE == 3 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 28, *reinterpret_cast<const uint32_t(*)[4]>(w3 + 4));
             } else {
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
