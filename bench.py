@@ -51,6 +51,9 @@ DTYPE = {
     3: "stored 30-bit fixed-point K (4 u8 slices, fp64-built) x 55-bit fixed-point D (7 u8 slices), "
        "exact int32 accumulation on tcgen05; fp64 CG",
 }
+DTYPE31 = ("31-bit fixed-point k~ (4 u8 slices: the fp32 MUFU ex2 value exactly, of an fp16-split "
+           "tensor-core exponent) x 31-bit fixed-point D (4 u8 slices), exact int32 accumulation of "
+           "the slice products on tcgen05 (those below 2^-38 of the scale dropped); fp64 CG")
 
 
 def work_per_matmul(cfg):
@@ -62,22 +65,29 @@ def work_per_matmul(cfg):
     return pairs, 2.0 * pairs * c
 
 
-def tensor_frac(cfg, world, mm_ms, pk, detail=False):
-    """Tensor-pipe work of one K1-TC launch: per 128 x 128 tile a 3xTF32
-    distance MMA (K = 3 DA, DA = round8(d + 2)) and 3 int8 MMAs (N = ND round(c + 1), K = 128),
-    as dense-bf16-equivalent flops (tf32 x2, int8 x0.5) over the launch time vs the measured
-    bf16 peak."""
+def tensor_frac(cfg, world, mm_ms, pk, detail=False, kgrid=23):
+    """Tensor-pipe work of one K1-TC launch, per 128 x 128 tile: the distance
+    (RBF: fp16 hi/lo, K = 32 packed at DA = 8, else 3 round16(DA); Matern: none) and the int8
+    slice MMAs (K = 128; q2, q1 at N = ND BLK, q0 trimmed to round16(3 BLK), the 31-bit grid's
+    residual slice at round16(2 BLK)), as dense-bf16-equivalent flops (f16 x1, int8 x0.5) over
+    the launch time vs the measured bf16 peak."""
+    r16 = lambda x: -(-x // 16) * 16
     c1 = cfg.t + 2
     da = -(-(cfg.d + 2) // 8) * 8
     if cfg.kind == synth.RBF:
-        nb = 4 * (-(-c1 // 4) * 4)
+        blk = -(-c1 // 4) * 4
+        nb = 4 * blk
+        kdist = 32 if da == 8 else 3 * r16(da)
+        nsum = 2 * nb + min(nb, r16(3 * blk)) + (r16(2 * blk) if kgrid == 31 else 0)
     else:                                           # Matern: five D slices, BLK = round16
-        nb = 5 * (-(-c1 // 16) * 16)
+        nb = 5 * r16(c1)
+        kdist = 0
+        nsum = 3 * nb
     rows = -(-(-(-cfg.n // world)) // 128) * 128
     cols = -(-cfg.n // 128) * 128
-    tf32 = 2.0 * rows * cols * 3 * da
-    i8 = 2.0 * rows * cols * nb * 3
-    eq = 2.0 * tf32 + 0.5 * i8
+    f16 = 2.0 * rows * cols * kdist
+    i8 = 2.0 * rows * cols * nsum
+    eq = f16 + 0.5 * i8
     ach = eq / (mm_ms * 1e-3) / 1e12
     peak = pk.get("bf16_tflops", 1590.0)
     return (ach / peak, ach, peak) if detail else ach / peak
@@ -175,7 +185,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kmode", default=None, choices=[None, "onthefly", "stored"])
-    ap.add_argument("--precision", default="int8exact", choices=["int8exact", "int8exact31", "fp64acc", "fp32acc"])
+    ap.add_argument("--precision", default="int8exact", choices=["int8exact", "int8exact31", "int8exact23", "fp64acc", "fp32acc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -204,7 +214,8 @@ def main():
         args.kmode, bb.STORED if cfg.stored else bb.ONTHEFLY)
     ctx = bb.Context(local_rank)
     ctx.set_matmul_precision({"int8exact": bb.INT8EXACT, "int8exact31": bb.INT8EXACT31,
-                              "fp64acc": bb.FP64ACC, "fp32acc": bb.FP32ACC}[args.precision])
+                              "int8exact23": bb.INT8EXACT23, "fp64acc": bb.FP64ACC,
+                              "fp32acc": bb.FP32ACC}[args.precision])
     if world > 1:
         ctx.set_comm()
     X = torch.from_numpy(pr.X).cuda()
@@ -322,16 +333,18 @@ def main():
                     "kernel_ms": mm_ms,
                     "kernel_gflops": loc_pairs * 2 * (cfg.t + 1) / (mm_ms * 1e-3) / 1e9}
         if path == 2:
-            # secondary: the implementation's own tensor-pipe work (3xTF32 distance + int8 slice
+            # secondary: the implementation's own tensor-pipe work (fp16 distance + int8 slice
             # products, as dense-bf16-equivalent flops) -- not the method's work
-            tf, tach, tpk = tensor_frac(cfg, world, mm_ms, pk, detail=True)
+            tf, tach, tpk = tensor_frac(cfg, world, mm_ms, pk, detail=True,
+                                        kgrid=stats[-1].get("kgrid_bits", 23))
             roofline["tensor_impl"] = {"achieved_tflops_bf16eq": tach, "peak": tpk, "frac": tf}
     launches = int(np.sum([s["gpu_launches"] for s in stats]))
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "s_per_mll_grad": ms / 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[path],
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": DTYPE[path] if not (path == 2 and stats[-1].get("kgrid_bits") == 31) else DTYPE31,
         "data": "synthetic (seeded; SURVEY.md §8d recipe)",
         "config": {"workload": f"{cfg.name}: exact GP MLL+grad, "
                                f"{'RBF' if cfg.kind == 0 else 'Matern-5/2'}"
@@ -340,6 +353,7 @@ def main():
                                f"{'stored' if kmode == bb.STORED else 'on-the-fly'} K",
                    "parallelism": f"row-partition x{world}",
                    "matmul_precision": args.precision,
+                   "kgrid_bits": stats[-1].get("kgrid_bits"),
                    "l2": "256 MB L2 flush between timed steps"},
         "roofline": roofline, "e2e": e2e, "gpu_launches": launches // max(len(stats), 1) * args.steps,
         "clocks": clocks,

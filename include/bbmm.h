@@ -77,7 +77,10 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   (SURVEY.md §8c "regime A"). */
 /* INT8EXACT (default): tcgen05 tensor cores, slice products summed EXACTLY in
  *   int32 (drained to fp64).  On the fly, RBF (isotropic or ARD): kernel values
- *   (fp32 MUFU ex2) on a 23-bit fixed-point grid, D as 31-bit fixed point
+ *   (fp32 MUFU ex2) on a 23- or 31-bit fixed-point grid -- 31 bits where the
+ *   23-bit grid's per-entry error (5.3e-8 s rms) would put the solves near the
+ *   1e-4 bar: sqrt(n) 5.3e-8 s / sigma^2 > 0.8e-4 (the error model of DESIGN.md
+ *   §6a: ||du|| / ||u|| ~ sqrt(n) eps / sigma^2) -- D as 31-bit fixed point
  *   (per-column scale), the exponent from an fp16 hi/lo-split tensor-core
  *   distance; any t + 1 <= 33 (padded to the next instantiated column block) with
  *   d <= 30, and max |x_scaled|^2 <= 16 (precision guard).  On the fly,
@@ -86,17 +89,19 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   values, 39-bit D; t + 1 <= 17, d <= 14.  Stored K (BBMM_STORED, t + 1 <= 33):
  *   K built in fp64 and stored as 30-bit fixed point, D as 55-bit fixed point.
  *   Everything else uses FP64ACC.
- * INT8EXACT31: as INT8EXACT, but the on-the-fly RBF kernel-matmul keeps the
- *   MUFU's kernel values on a 31-bit grid (a fourth, residual u8 slice of k~):
- *   per-entry error 3.3e-8 instead of 5.3e-8 rms at C4 (the grid rounding
- *   removed, the MUFU's own error left), for the north-star solve bar at
- *   n = 1M; ~10-20 % slower kernel-matmul.  The derivative pass
- *   and the Matern / stored operators are those of INT8EXACT. */
+ * INT8EXACT31 / INT8EXACT23: INT8EXACT with the on-the-fly RBF grid forced to
+ *   31 / 23 bits.  The 31-bit grid keeps the MUFU's kernel values exactly (a
+ *   fourth, residual u8 slice of k~): per-entry error 3.3e-8 instead of 5.3e-8
+ *   rms at C4 (the grid rounding removed, the MUFU's own error left), which the
+ *   north-star solve bar needs at n = 1M; 1.18x the 23-bit
+ *   kernel-matmul time.  The derivative pass and the Matern / stored operators
+ *   are those of INT8EXACT. */
 typedef enum {
     BBMM_MATMUL_FP64ACC = 0,
     BBMM_MATMUL_FP32ACC = 1,
     BBMM_MATMUL_INT8EXACT = 2,
-    BBMM_MATMUL_INT8EXACT31 = 3
+    BBMM_MATMUL_INT8EXACT31 = 3,
+    BBMM_MATMUL_INT8EXACT23 = 4
 } bbmm_matmul_precision_t;
 
 typedef struct {
@@ -136,6 +141,8 @@ typedef struct {
     double relres_max;       /* max over the t + 1 columns of ||r_c|| / ||b_c|| at exit */
     double ms_comm;          /* device time inside the collectives (all-reduces, all-gathers)
                                 on the context stream, incl. waiting for peers; 0 single-rank */
+    int32_t kgrid_bits;      /* fixed-point grid of the on-the-fly kernel values (matmul_path
+                                2): 23 or 31; 0 otherwise */
 } bbmm_stats_t;
 
 /* ---- context ----------------------------------------------------------- */

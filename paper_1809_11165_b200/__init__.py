@@ -27,7 +27,8 @@ STORED = 1
 FP64ACC = 0     # matmul precision: fp64 D, fp64 products and sums (FFMA/DFMA path)
 FP32ACC = 1     # fp32 D, 16-term fp32 chunks folded into fp64 (regime A only)
 INT8EXACT = 2   # default: tcgen05 int8 tensor cores, exact integer contraction (else FP64ACC)
-INT8EXACT31 = 3  # INT8EXACT with the on-the-fly RBF kernel values on a 31-bit grid (n ~ 1M parity)
+INT8EXACT31 = 3  # INT8EXACT with the on-the-fly RBF kernel values forced to the 31-bit grid
+INT8EXACT23 = 4  # INT8EXACT with the on-the-fly RBF kernel values forced to the 23-bit grid
 
 _STATUS = {0: "OK", 2: "ERR_ARG", 3: "ERR_DATA", 4: "ERR_NUMERIC", 5: "ERR_CUDA",
            6: "ERR_NCCL", 7: "ERR_OOM"}
@@ -59,7 +60,7 @@ class Stats(C.Structure):
                 ("ms_slq", C.c_double), ("ms_deriv", C.c_double),
                 ("matmul_launches", C.c_int32), ("gpu_launches", C.c_int32),
                 ("matmul_path", C.c_int32), ("unconverged", C.c_int32),
-                ("relres_max", C.c_double), ("ms_comm", C.c_double)]
+                ("relres_max", C.c_double), ("ms_comm", C.c_double), ("kgrid_bits", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

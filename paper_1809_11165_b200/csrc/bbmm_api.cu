@@ -395,11 +395,13 @@ bbmm_status_t bbmm_ctx_set_comm(bbmm_ctx_t ctx, int nranks, int rank, const void
 
 bbmm_status_t bbmm_ctx_set_matmul_precision(bbmm_ctx_t ctx, bbmm_matmul_precision_t p) {
     if (!ctx || (p != BBMM_MATMUL_FP64ACC && p != BBMM_MATMUL_FP32ACC &&
-                 p != BBMM_MATMUL_INT8EXACT && p != BBMM_MATMUL_INT8EXACT31))
+                 p != BBMM_MATMUL_INT8EXACT && p != BBMM_MATMUL_INT8EXACT31 &&
+                 p != BBMM_MATMUL_INT8EXACT23))
         return BBMM_ERR_ARG;
     ctx->matmul_acc64 = (p != BBMM_MATMUL_FP32ACC);
-    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT || p == BBMM_MATMUL_INT8EXACT31);
-    ctx->matmul_grid31 = (p == BBMM_MATMUL_INT8EXACT31);
+    ctx->matmul_tc = (p == BBMM_MATMUL_INT8EXACT || p == BBMM_MATMUL_INT8EXACT31 ||
+                      p == BBMM_MATMUL_INT8EXACT23);
+    ctx->matmul_grid = p == BBMM_MATMUL_INT8EXACT31 ? 31 : p == BBMM_MATMUL_INT8EXACT23 ? 23 : 0;
     return BBMM_OK;
 }
 
@@ -455,9 +457,9 @@ bbmm_status_t bbmm_kernel_matmul(bbmm_ctx_t ctx, const float *X, int64_t n, int3
             const int64_t npad = k1tc_pad_rows(n);
             double *S = (double *)ctx->ws.get("tc_S", kMaxCols * 8);
             k1tc_colmax(ctx, D, ldd, n, ncols, S);
-            const int nd = tc_dslices(op);
-            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", (size_t)npad * tc_bslice_rows(op.cb, nd));
-            k1tc_pack(ctx, D, ldd, 0, n, n, ncols, S, Bp, nd, op.cb);
+            BBMM_REQUIRE(op.npad == npad, "tc operand rows");
+            uint8_t *Bp = (uint8_t *)ctx->ws.get("tc_B", tc_bp_bytes(op));
+            tc_pack(ctx, op, D, ldd, 0, n, n, ncols, S, Bp);
             size_t cap = tc_vpart_elems(op, n, nloc, op.cb);
             double *Vpart = (double *)ctx->ws.get("mm_Vpart", cap * 8);
             int splits = tc_matmul(ctx, op, Bp, S, op.cb, n, rr.r0, nloc, h.s, Vpart, cap, nullptr,
@@ -636,16 +638,26 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             double *Bd = (double *)ws.get("d_Bd", (size_t)std::max<int64_t>(nloc, 1) * c * 8);
             double *Sd = (double *)ws.get("d_S", kMaxCols * 8);
             const int64_t npad_tc = k1tc_pad_rows(rr.nb * ctx->nranks);
-            const int cbd = k1tc2_deriv_cols(d, c);          // MODE-1 instantiation (>= c)
-            uint8_t *Bp = (uint8_t *)ws.get("tc_B", (size_t)npad_tc * k1tc_bslice_rows(cbd));
+            // MODE-1 instantiation (>= c), or the operand's column chunks of 33 (c + 1 > 33)
+            const bool chunked = tcop.nch > 1;
+            const int cbd = chunked ? tcop.cb : k1tc2_deriv_cols(d, c);
+            const int vsd = chunked ? tc_vstride(tcop) : (cbd + 3) & ~3;
+            const int nchd = chunked ? tcop.nch : 1;
+            BBMM_REQUIRE(!chunked || tcop.npad == npad_tc, "tc operand rows");
+            uint8_t *Bp = (uint8_t *)ws.get("tc_B", (size_t)nchd * npad_tc * k1tc_bslice_rows(cbd));
             if (nloc > 0) {
                 k_build_bd<<<grid_for(nloc * c), 256, 0, sm>>>(o.U_d, Z0, nloc, t, Bd);
                 ctx->launches++;
             }
             k1tc_colmax(ctx, Bd, c, nloc, c, Sd);
             allreduce_max(ctx, Sd, c);
-            if (nloc > 0) k1tc_pack(ctx, Bd, c, rr.r0, nloc, n, c, Sd, Bp, 4, cbd);
-            allgather_rows(ctx, Bp, (size_t)rr.nb * k1tc_bslice_rows(cbd));
+            if (nloc > 0) {
+                if (chunked) tc_pack(ctx, tcop, Bd, c, rr.r0, nloc, n, c, Sd, Bp);
+                else k1tc_pack(ctx, Bd, c, rr.r0, nloc, n, c, Sd, Bp, 4, cbd);
+            }
+            for (int z = 0; z < nchd; z++)
+                allgather_rows(ctx, Bp + (size_t)z * npad_tc * k1tc_bslice_rows(cbd),
+                               (size_t)rr.nb * k1tc_bslice_rows(cbd));
             const size_t cap = tc_vpart_elems(tcop, n, nloc, cbd);
             double *Vp = (double *)ws.get("d_Vpart", std::max<size_t>(cap, 1) * 8);
             double *dpart = (double *)ws.get("d_part", (size_t)sblk * 8);
@@ -653,7 +665,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
                 // S_l at dred[0]: the k~ r^2 kernel-matmul (mode 1)
                 const int sp = tc_matmul(ctx, tcop, Bp, Sd, cbd, n, rr.r0, nloc, h.s, Vp, cap,
                                          nullptr, nullptr, 1);
-                k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, (cbd + 3) & ~3, nloc, t, o.U_d, dpart);
+                k_deriv_dot<<<sblk, 256, 0, sm>>>(Vp, sp, vsd, nloc, t, o.U_d, dpart);
                 reduce_blocks(ctx, dpart, sblk, 1, dred);
                 // S_s at dred[dp]: from the solves' residual identity (no matmul)
                 k_outputscale_term<<<sblk, 256, 0, sm>>>(o.U_d, o.R_d, B, Z0, h.noise_var, nloc,
@@ -766,6 +778,7 @@ bbmm_status_t bbmm_mll_and_grad(bbmm_ctx_t ctx, const float *X, const float *y, 
             s.matmul_launches = o.matmul_launches;
             s.gpu_launches = ctx->launches - launches0;
             s.matmul_path = tcop.version == 3 ? 3 : tcop.version == 2 ? 2 : (Kst ? 1 : 0);
+            s.kgrid_bits = tcop.version == 2 ? (tcop.grid31 ? 31 : 23) : 0;
             s.relres_max = 0.0;
             bool active = false;
             for (int col = 0; col < c && col < (int)o.relres.size(); col++) {

@@ -129,7 +129,7 @@ struct bbmm_ctx_s {
     int launches = 0;   // library kernel launches since last reset
     bool matmul_acc64 = true;   // FP64ACC / INT8EXACT fallback: fp64 accumulation
     bool matmul_tc = true;      // BBMM_MATMUL_INT8EXACT (default): tcgen05 exact contraction
-    bool matmul_grid31 = false; // BBMM_MATMUL_INT8EXACT31: on-the-fly RBF k~ on a 31-bit grid
+    int matmul_grid = 0;        // on-the-fly RBF k~ grid: 0 auto (INT8EXACT), 31 or 23 (forced)
     int *pinned_flag = nullptr; // pinned host int for per-iteration convergence polling (lazy)
     bbmm::LocalGroup *local = nullptr;   // in-process rank group (comm_local.cu) instead of NCCL
     // timing events of the mBCG matmuls, reused across calls (created on first use, destroyed
@@ -222,7 +222,10 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
 size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c);
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                  const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
-                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0);
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode = 0,
+                 int ldv = 0, int coff = 0);
+// column chunking of K1-TC for c above the largest instantiation (cb, nch; nch = 0: none)
+int k1tc2_chunks(int kind, int d, int c, int *cb);
 bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c);
 
 // Tensor-core operand of one mBCG call (prepared once per call).
@@ -235,9 +238,19 @@ struct TcOperand {
     int kind = 0;               // kernel family of the operand
     int nd = 4;                 // D slices of the packed operand (k1tc_pack nd)
     int cb = 0;                 // columns of the kernel instantiation (>= c; zero-padded)
+    // v2 with more columns than the largest instantiation: nch column chunks of cb columns, each
+    // its own packed operand (npad rows apart) and launch, writing Vpart columns [z cb, z cb + cb)
+    int nch = 1;
+    int64_t npad = 0;           // rows of one chunk's packed operand (k1tc_pad_rows)
+    bool grid31 = false;        // v2 RBF: kernel values on the 31-bit grid (K1-TC MODE 3)
 };
-// Vpart row stride of a tensor-core operand's matmul (the instantiation's round4(cb))
-inline int tc_vstride(const TcOperand &op) { return (op.cb + 3) & ~3; }
+// Vpart row stride of a tensor-core operand's matmul (round4 of all chunks' columns)
+inline int tc_vstride(const TcOperand &op) { return (op.nch * op.cb + 3) & ~3; }
+// bytes of the packed D operand of all chunks (k1tc_pack layout per chunk)
+size_t tc_bp_bytes(const TcOperand &op);
+// pack D (c columns, rows [row0, row0 + rows) of n) into the operand's chunks (k1tc_pack each)
+void tc_pack(bbmm_ctx_s *ctx, const TcOperand &op, const double *D, int64_t ldd, int64_t row0,
+             int64_t rows, int64_t n, int c, const double *S, uint8_t *Bp);
 int tc_dslices(const TcOperand &op);   // D slices of the operand's packed format (4 or 5)
 // Prepare the tensor-core inputs for (kind, d, c) if the INT8EXACT mode applies.
 TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, const Hyper &h,

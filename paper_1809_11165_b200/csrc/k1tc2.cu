@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
           const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
           int64_t nloc, int64_t tiles_per_split, int64_t ntiles, double s,
-          double *__restrict__ Vpart) {
+          double *__restrict__ Vpart, int ldv, int coff) {
     constexpr int ND = MODE == 2 ? 5 : 4;
     using K = Cfg<C, DA, ND>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -693,16 +693,18 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         }
         if (DEFER && ntl > 0) publish(ntl - 1);
         if (h == 0 && valid) {
+            // Vpart rows of ldv columns, this launch's block at column coff (column chunks)
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
-            double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * CS;
+            double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * ldv + coff;
             const double base = s * (ND == 4 ? 0x1p-53 : 0x1p-61) *
                                 (MODE == 1 ? 1.3862943611198906 : 1.0);   // MODE 1: r^2 = -2 ln2 S
             const double cacc = acc_sm[C][rl];
 #pragma unroll
             for (int c = 0; c < C; c++) out[c] = base * Sc[c] * (acc_sm[c][rl] - cacc);
+            if (coff + CS <= ldv)
 #pragma unroll
-            for (int c = C; c < CS; c++) out[c] = 0.0;
+                for (int c = C; c < CS; c++) out[c] = 0.0;
         }
     }
     ptx::tc_fence_before();
@@ -820,6 +822,16 @@ int k1tc2_cols(int kind, int d, int c) {
     return c <= 11 ? 11 : c <= 17 ? 17 : c <= 33 ? 33 : 0;
 }
 bool k1tc2_supported(int kind, int d, int c) { return k1tc2_cols(kind, d, c) > 0; }
+// More columns than the largest instantiation (c + 1 > 33 RBF / 17 Matern, up to the C-ABI's 64):
+// ceil(c / cb) column chunks of the largest block, one launch each.  Every chunk recomputes the
+// kernel values (the MUFU-bound pair loop runs nch times) -- still well under the CUDA-core
+// FP64ACC path, whose cost grows with c (VERDICT r1 "next" 7).
+int k1tc2_chunks(int kind, int d, int c, int *cb) {
+    const int big = kind == BBMM_MATERN52 ? 17 : 33;
+    if (c <= big || k1tc2_cols(kind, d, big) != big) return 0;
+    *cb = big;
+    return (c + big - 1) / big;
+}
 // isotropic-RBF derivative (MODE 1) instantiations: C in {11, 17, 33}, any da <= 32
 int k1tc2_deriv_cols(int d, int c) {
     if (tc2_da(d) > 32) return 0;
@@ -859,14 +871,15 @@ float k1tc2_prep_inputs(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, const
 template <int C, int DA, int MODE, int DM = DA>
 static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                       const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
-                      double *Vpart, size_t cap) {
+                      double *Vpart, size_t cap, int ldv, int coff) {
     using K = tc2::Cfg<C, DA, MODE == 2 ? 5 : 4>;
     const int64_t ntiles = ceil_div(n, tc2::BK);
     const int64_t rb = ceil_div(nloc, tc2::BM);
     int64_t sp = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, rb), ntiles));
     const int64_t tps = ceil_div(ntiles, sp);
     sp = ceil_div(ntiles, tps);
-    BBMM_REQUIRE((size_t)sp * nloc * ((C + 3) & ~3) <= cap, "Vpart workspace too small (k1tc2)");
+    if (ldv == 0) ldv = (C + 3) & ~3;
+    BBMM_REQUIRE(coff + C <= ldv && (size_t)sp * nloc * ldv <= cap, "Vpart workspace too small (k1tc2)");
     static DeviceOnce attr;
     attr(ctx->device, [] {
         BBMM_CUDA(cudaFuncSetAttribute(tc2::k1tc2_rbf<C, DA, MODE, DM>,
@@ -874,7 +887,7 @@ static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const u
     });
     dim3 grid((unsigned)rb, (unsigned)sp);
     tc2::k1tc2_rbf<C, DA, MODE, DM><<<grid, tc2::kThreads, K::SMEM, ctx->stream>>>(
-        Xa, XB, Bp, S, r0, nloc, tps, ntiles, s, Vpart);
+        Xa, XB, Bp, S, r0, nloc, tps, ntiles, s, Vpart, ldv, coff);
     BBMM_LAUNCH_CHECK();
     ctx->launches++;
     return (int)sp;
@@ -888,12 +901,15 @@ size_t k1tc2_vpart_elems(int64_t n, int64_t nloc, int c) {
 }
 
 bool k1tc2_deriv_supported(int kind, int n_ls, int d, int c) {
-    return n_ls == 1 && kind == BBMM_RBF && k1tc2_deriv_cols(d, c) > 0;
+    int cb;
+    return n_ls == 1 && kind == BBMM_RBF &&
+           (k1tc2_deriv_cols(d, c) > 0 || k1tc2_chunks(kind, d, c, &cb) > 0);   // chunks: MODE 1 at 33
 }
 
 int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                  const double *S, int d, int c, int64_t n, int64_t r0, int64_t nloc, double s,
-                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode) {
+                 double *Vpart, size_t cap, cudaEvent_t ev0, cudaEvent_t ev1, int mode, int ldv,
+                 int coff) {
     if (ev0) record_event(ctx, ev0);
     int sp = 1;
     const int da = tc2_da(d);
@@ -901,7 +917,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         BBMM_REQUIRE(k1tc2_deriv_cols(d, c) == c, "k1tc2: derivative mode shape");
         if (nloc > 0) {
 #define BBMM_TC2D(CC, DD) \
-    if (c == CC && da == DD) sp = launch_tc2<CC, DD, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
+    if (c == CC && da == DD) sp = launch_tc2<CC, DD, 1>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff); else
             BBMM_TC2D(11, 8) BBMM_TC2D(11, 16) BBMM_TC2D(11, 24) BBMM_TC2D(11, 32)
             BBMM_TC2D(17, 8) BBMM_TC2D(17, 16) BBMM_TC2D(17, 24) BBMM_TC2D(17, 32)
             BBMM_TC2D(33, 8) BBMM_TC2D(33, 16) BBMM_TC2D(33, 24) BBMM_TC2D(33, 32)
@@ -913,20 +929,20 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
     }
     if (mode == 2) {   // Matern-5/2
         if (nloc > 0) {
-            if (c == 17 && d == 9) sp = launch_tc2<17, 16, 2, 9>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
-            else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap);
+            if (c == 17 && d == 9) sp = launch_tc2<17, 16, 2, 9>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
+            else if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
+            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
+            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
+            else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
             else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported Matern shape"};
         }
         if (ev1) record_event(ctx, ev1);
         return sp;
     }
 #define BBMM_TC2(CC, DD) \
-    if (c == CC && da == DD) sp = g31 ? launch_tc2<CC, DD, 3>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap) \
-                                      : launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap); else
-    const bool g31 = ctx->matmul_grid31;   // INT8EXACT31: MODE 3 (31-bit k~ grid)
+    if (c == CC && da == DD) sp = g31 ? launch_tc2<CC, DD, 3>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff) \
+                                      : launch_tc2<CC, DD, 0>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff); else
+    const bool g31 = mode == 3;   // the 31-bit k~ grid (TcOperand::grid31): MODE 3
     if (nloc > 0) {
         BBMM_TC2(1, 8) BBMM_TC2(2, 8) BBMM_TC2(4, 8) BBMM_TC2(8, 8) BBMM_TC2(11, 8)
         BBMM_TC2(17, 8) BBMM_TC2(1, 16) BBMM_TC2(2, 16) BBMM_TC2(4, 16) BBMM_TC2(8, 16)
@@ -947,7 +963,9 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
     if (!ctx->matmul_tc) return op;
     const int64_t npad = k1tc_pad_rows(npad_rows);
     op.d = d;
-    if (k1tc2_supported(h.kind, d, c)) {
+    int cbk = 0;
+    const int nch = k1tc2_chunks(h.kind, d, c, &cbk);
+    if (k1tc2_supported(h.kind, d, c) || nch > 0) {
         float *xa = (float *)ctx->ws.get("tc2_Xa", (size_t)k1tc2_xa_floats(npad, d) * 4);
         float *xb = (float *)ctx->ws.get("tc2_XB", (size_t)k1tc2_xb_floats(npad, d) * 4);
         const float max_sq = k1tc2_prep_inputs(ctx, X, n, d, h, xa, xb, npad);
@@ -959,7 +977,16 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         op.version = 2;
         op.kind = h.kind;
         op.nd = h.kind == BBMM_MATERN52 ? 5 : 4;
-        op.cb = k1tc2_cols(h.kind, d, c);
+        op.cb = nch > 0 ? cbk : k1tc2_cols(h.kind, d, c);
+        op.nch = nch > 0 ? nch : 1;
+        op.npad = npad;
+        // k~ grid: the 23-bit grid's per-entry error (5.3e-8 s rms at C4, the
+        // MUFU's 2.8e-8 random part plus the grid's 4.2e-8) moves the solves by about
+        // sqrt(n) eps s / sigma^2; where that would pass 0.8e-4 (a 20 % margin under the 1e-4
+        // bar) the 31-bit grid (MUFU error only, 3.3e-8) is used -- C4 at n = 1M: 1.77e-4 -> 31 bits
+        const double est23 = std::sqrt((double)n) * 5.3e-8 * h.s / h.noise_var;
+        op.grid31 = h.kind == BBMM_RBF &&
+                    (ctx->matmul_grid == 31 || (ctx->matmul_grid == 0 && est23 > 0.8e-4));
         op.Xa = xa;
         op.XB = xb;
     }
@@ -967,7 +994,22 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
 }
 
 size_t tc_vpart_elems(const TcOperand &op, int64_t n, int64_t nloc, int cb) {
-    return op.version == 3 ? k2tc_vpart_elems(n, nloc, cb) : k1tc2_vpart_elems(n, nloc, cb);
+    if (op.version == 3) return k2tc_vpart_elems(n, nloc, cb);
+    return k1tc2_vpart_elems(n, nloc, cb == op.cb ? op.nch * op.cb : cb);   // all chunks' columns
+}
+
+size_t tc_bp_bytes(const TcOperand &op) {
+    return (size_t)op.nch * op.npad * tc_bslice_rows(op.cb, tc_dslices(op));
+}
+
+void tc_pack(bbmm_ctx_s *ctx, const TcOperand &op, const double *D, int64_t ldd, int64_t row0,
+             int64_t rows, int64_t n, int c, const double *S, uint8_t *Bp) {
+    const int nd = tc_dslices(op);
+    const size_t stride = (size_t)op.npad * tc_bslice_rows(op.cb, nd);
+    for (int z = 0; z < op.nch; z++) {
+        const int c0 = z * op.cb, cz = std::min(op.cb, c - c0);
+        k1tc_pack(ctx, D + c0, ldd, row0, rows, n, cz, S + c0, Bp + z * stride, nd, op.cb);
+    }
 }
 
 int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const double *S, int c,
@@ -981,6 +1023,16 @@ int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const dou
     if (op.kind == BBMM_MATERN52) {
         BBMM_REQUIRE(mode == 0, "k1tc2: no Matern derivative mode");
         mode = 2;
+    }
+    if (mode == 0 && op.grid31) mode = 3;   // the blackbox matmul on the 31-bit k~ grid
+    if (op.nch > 1 && c == op.cb) {      // column chunks (tc_pack layout; mbcg and derivative)
+        const size_t stride = (size_t)op.npad * tc_bslice_rows(op.cb, tc_dslices(op));
+        int sp = 0;
+        for (int z = 0; z < op.nch; z++)
+            sp = k1tc2_matmul(ctx, op.Xa, op.XB, Bp + z * stride, S + z * op.cb, op.d, c, n, r0,
+                              nloc, s, Vpart, cap, z == 0 ? ev0 : nullptr,
+                              z + 1 == op.nch ? ev1 : nullptr, mode, tc_vstride(op), z * op.cb);
+        return sp;
     }
     return k1tc2_matmul(ctx, op.Xa, op.XB, Bp, S, op.d, c, n, r0, nloc, s, Vpart, cap, ev0, ev1,
                         mode);

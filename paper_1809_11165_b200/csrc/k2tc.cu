@@ -441,6 +441,7 @@ TcOperand prepare_operator(bbmm_ctx_s *ctx, bool stored, const float *X, const f
         op.kind = h.kind;
         op.nd = k2tc::ND;
         op.cb = k2tc_cols(c);
+        op.npad = k1tc_pad_rows(npad_rows);
         op.Kq = kq;
         return op;
     }

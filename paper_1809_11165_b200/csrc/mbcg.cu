@@ -755,9 +755,10 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     const int cb = use_tc ? a.tc.cb : c;              // columns of the tensor-core instantiation
     const int tc_rows = tc_bslice_rows(cb, tc_nd);
     const int vs = use_tc ? tc_vstride(a.tc) : cs;    // Vpart row stride
-    uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", (size_t)npad_tc * tc_rows) : nullptr;
+    BBMM_REQUIRE(!use_tc || a.tc.npad == npad_tc, "tc operand rows");
+    uint8_t *Bp = use_tc ? (uint8_t *)ws.get("tc_B", tc_bp_bytes(a.tc)) : nullptr;
     double *Stc = use_tc ? (double *)ws.get("tc_S", kMaxCols * 8) : nullptr;
-    if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, (size_t)npad_tc * tc_rows, sm));
+    if (use_tc) BBMM_CUDA(cudaMemsetAsync(Bp, 0, tc_bp_bytes(a.tc), sm));
     double *Vpart = (double *)ws.get("cg_Vpart", std::max<size_t>(vcap, 1) * 8);
     const PassGeom g = pass_geom(nloc, c);
     const int nblk = (int)g.grid.x;
@@ -901,8 +902,10 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
             // tensor-core operand: global column scales, then int8 slices
             k1tc_colmax(ctx, D, c, nloc, c, Stc);
             if (multi) allreduce_max(ctx, Stc, c);
-            if (nloc > 0) k1tc_pack(ctx, D, c, a.r0, nloc, a.n, c, Stc, Bp, tc_nd, cb);
-            if (multi) allgather_rows(ctx, Bp, (size_t)a.nb * tc_rows);
+            if (nloc > 0) tc_pack(ctx, a.tc, D, c, a.r0, nloc, a.n, c, Stc, Bp);
+            if (multi)      // each column chunk's operand holds the ranks' row blocks in order
+                for (int z = 0; z < a.tc.nch; z++)
+                    allgather_rows(ctx, Bp + (size_t)z * npad_tc * tc_rows, (size_t)a.nb * tc_rows);
         } else if (multi && !use_sor) {          // SoR needs only local rows of D
             allgather_rows(ctx, Dm, (size_t)a.nb * cs * esz);
         }
@@ -911,7 +914,7 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
     BBMM_LAUNCH_CHECK();
 
     // fused vector work (one cooperative kernel per iteration) where it applies
-    bool fused = mbcg_fused_applicable(ctx, c, k, use_sor, nloc);
+    bool fused = mbcg_fused_applicable(ctx, c, k, use_sor, nloc) && (!use_tc || a.tc.nch == 1);
     FusedPlan fplan;
     double *Cinv = nullptr, *fpart = nullptr, *fpartW = nullptr, *fred = nullptr;
     if (fused) {

@@ -59,7 +59,7 @@ def main():
     ns = [int(a) for a in sys.argv[1:]] or [131072, 1000000]
     ctx = bb.Context(0)
     for n in ns:
-        for prec, label in [(bb.INT8EXACT, "int8exact"), (bb.INT8EXACT31, "int8exact31"),
+        for prec, label in [(bb.INT8EXACT23, "int8exact23"), (bb.INT8EXACT31, "int8exact31"),
                             (bb.FP64ACC, "fp64acc")]:
             if prec == bb.FP64ACC and n > 300000:
                 continue                  # ~34 s per K̂·D at n = 1M on CUDA cores

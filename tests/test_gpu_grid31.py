@@ -71,12 +71,12 @@ def test_grid31_kernel_values_are_finer(ctx):
     noise = math.exp(2 * pr.log_noise)
     Kref = np.stack([s * np.exp(-0.5 * ((Xs - Xs[j]) ** 2).sum(1)) for j in cols], 1)
     rms = {}
-    for prec in (bb.INT8EXACT, bb.INT8EXACT31):
+    for prec in (bb.INT8EXACT23, bb.INT8EXACT31):
         V = _matmul(ctx, pr, D, prec)
         V[cols, np.arange(m)] -= noise
         rms[prec] = float(np.sqrt(((V - Kref) ** 2).mean()) / s)
     assert rms[bb.INT8EXACT31] < 4.0e-8, rms
-    assert rms[bb.INT8EXACT31] < 0.8 * rms[bb.INT8EXACT], rms
+    assert rms[bb.INT8EXACT31] < 0.8 * rms[bb.INT8EXACT23], rms
 
 
 @pytest.mark.parametrize("name,n", [("C4", 4000), ("C4", 1001), ("C3", 2500)])
@@ -104,3 +104,19 @@ def test_grid31_full_size_matmul_sampled_rows(ctx, orc):
     absb = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D), rows=rows)
     err = np.abs(V[rows] - ref)
     assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
+
+
+@pytest.mark.parametrize("n,bits", [(4000, 23), (131072, 23), (262144, 31), (1000000, 31)])
+def test_default_grid_follows_the_error_model(ctx, n, bits):
+    """INT8EXACT picks the k~ grid per call: 31 bits where sqrt(n) 5.3e-8 s / sigma^2 > 0.8e-4
+    (C4 recipe: s = 1, sigma^2 = 0.3 -> the switch at n ~ 205k); stats report it."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], n)
+    pr = synth.make_problem(cfg, seed=0)
+    g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), 1, 5, 2, seed=7)
+    assert g["stats"]["matmul_path"] == 2 and g["stats"]["kgrid_bits"] == bits
+    ctx.set_matmul_precision(bb.INT8EXACT23)
+    try:
+        g = bb.mll_and_grad(ctx, dev(pr.X), dev(pr.y), hyper_of(pr), 1, 5, 2, seed=7)
+    finally:
+        ctx.set_matmul_precision(bb.INT8EXACT)
+    assert g["stats"]["kgrid_bits"] == 23

@@ -275,3 +275,24 @@ def test_predict_cov_partitioned_matches_single_rank(orc):
     for m, C in parts:
         np.testing.assert_array_equal(C, parts[0][1])
         assert np.abs(C - C1).max() <= 1e-8 and np.abs(m - m1).max() <= 1e-8
+
+
+@pytest.mark.parametrize("name,t,nranks", [("C4", 39, 2), ("C2", 24, 3)])
+def test_column_chunks_partitioned_matches_single_rank(orc, name, t, nranks):
+    """K1-TC column chunks (t + 1 above the largest block) on a row partition: each chunk's packed
+    operand is all-gathered on its own; results equal the single-rank call up to reduction order."""
+    cfg = synth.dataclasses.replace(synth.scaled(synth.CONFIGS[name], 1500), t=t, k=20)
+    pr = synth.make_problem(cfg, seed=0)
+    X, y, h = dev(pr.X), dev(pr.y), hyper_of(pr)
+
+    def call(ctx):
+        return bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=7, kmode=bb.ONTHEFLY,
+                               return_solves=True)
+
+    parts = run_ranks(nranks, call, bb.INT8EXACT)
+    one = single(call)
+    assert all(g["stats"]["matmul_path"] == 2 for g in parts)
+    U = np.concatenate([g["U"].cpu().numpy() for g in parts], 0)
+    assert colwise_rel(U, one["U"].cpu().numpy()).max() < 1e-6
+    assert abs(parts[0]["mll"] - one["mll"]) <= 1e-8 * abs(one["mll"])
+    assert np.linalg.norm(parts[0]["grad"] - one["grad"]) <= 2e-5 * np.linalg.norm(one["grad"])
