@@ -571,28 +571,28 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 a1 = __byte_perm(t01, t23, 0x5410);      // H.b0: 2^16 (q1's)
                 a0 = __byte_perm(l01, l23, 0x7632);      // L.b1: 2^8  (q0's)
                 a3 = __byte_perm(l01, l23, 0x5410);      // L.b0: 2^0  (residual slot)
-                return;
+            } else {
+                // q = 2 + 2 k~ in [2, 4]: for k~ < 1 the exponent is 128 (bit 23 = 0) and the
+                // mantissa is k~ 2^23 rounded to nearest; k~ = 1 gives 4.0 = exponent 129, whose
+                // low bit lands on bit 23 = 2^23 = k~ 2^23 again.  So the three low bytes are
+                // exactly the 23-bit fixed-point k~ 2^23 for every k~ in [0, 1] (grid 2^-23: half
+                // the rounding of the q = 2 + k~ form).  Two points per instruction (FFMA2).
+    #pragma unroll
+                for (int v = 0; v < 4; v += 2) {
+                    unsigned long long pq;
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(pq) : "r"(q[v]), "r"(q[v + 1]));
+                    asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pq));
+                }
+                const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
+                const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
+                const uint32_t u01 = __byte_perm(q[0], q[1], 0x7351);
+                const uint32_t u23 = __byte_perm(q[2], q[3], 0x7351);
+                a0 = __byte_perm(t01, t23, 0x5410);
+                a2 = __byte_perm(t01, t23, 0x7632);
+                a1 = __byte_perm(u01, u23, 0x5410);
+                a3 = 0u;
             }
-            // q = 2 + 2 k~ in [2, 4]: for k~ < 1 the exponent is 128 (bit 23 = 0) and the
-            // mantissa is k~ 2^23 rounded to nearest; k~ = 1 gives 4.0 = exponent 129, whose
-            // low bit lands on bit 23 = 2^23 = k~ 2^23 again.  So the three low bytes are
-            // exactly the 23-bit fixed-point k~ 2^23 for every k~ in [0, 1] (grid 2^-23: half
-            // the rounding of the q = 2 + k~ form).  Two points per instruction (FFMA2).
-#pragma unroll
-            for (int v = 0; v < 4; v += 2) {
-                unsigned long long pq;
-                asm("mov.b64 %0, {%1, %2};" : "=l"(pq) : "r"(q[v]), "r"(q[v + 1]));
-                asm("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(pq) : "l"(0x4000000040000000ull));
-                asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pq));
-            }
-            const uint32_t t01 = __byte_perm(q[0], q[1], 0x6240);
-            const uint32_t t23 = __byte_perm(q[2], q[3], 0x6240);
-            const uint32_t u01 = __byte_perm(q[0], q[1], 0x7351);
-            const uint32_t u23 = __byte_perm(q[2], q[3], 0x7351);
-            a0 = __byte_perm(t01, t23, 0x5410);
-            a2 = __byte_perm(t01, t23, 0x7632);
-            a1 = __byte_perm(u01, u23, 0x5410);
-            a3 = 0u;
         };
         // publish tile tp's A slices (stores issued earlier), then drain the
         // accumulators if tp closed a window
