@@ -88,6 +88,18 @@ namespace tc2 {
 #ifndef BBMM_TC2_ABL
 #define BBMM_TC2_ABL 0
 #endif
+// S loaded in two tcgen05.ld.x16 halves, the second issued after the first half's quantisation
+// (a shorter TMEM load occupying the warp's MIO queue, where its MUFU ops also queue; measured:
+// MODE 3 339.6 -> 335.7 ms alone, but 336.9 with the store burst; MODE 0 +0.3 %) -- off
+#ifndef BBMM_TC2_SPLITLD
+#define BBMM_TC2_SPLITLD 0
+#endif
+// MODE 3: all A-slice stores of a tile as four tcgen05.st.x8 after the second half instead of
+// eight .x4 spread over the tile (measured: MODE 3 339.6 -> 332.3 ms at C4; MODE 0, whose
+// three slices are stored per half, gets slower with a burst: 289.0 -> 295.8 ms)
+#ifndef BBMM_TC2_STBURST
+#define BBMM_TC2_STBURST 1
+#endif
 #ifndef BBMM_TC2_TRIM
 #define BBMM_TC2_TRIM 1
 #endif
@@ -325,7 +337,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // MODE 3 residual slice r x [p3 p2 (p1)]: N = round16(2 BLK) -- the extra columns land
         // in blocks of their own weight (r p1 -> block 5) or, at BLK = 4, in the padding
         // column block 6 that is never drained (ACC_END >= 7 BLK there)
-        constexpr int NR = r16(2 * K::BLK);
+        constexpr int NR = r16(2 * K::BLK);   // (r x p3 alone, N = round16(BLK): no faster)
         static_assert(MODE != 3 || NR <= 3 * K::BLK || 7 * K::BLK <= K::ACC_END, "residual N");
         constexpr uint32_t IDQR = ptx::idesc_i8(BM, NR, false, false);
         const bool leader = ptx::elect_one();
@@ -657,6 +669,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&free_x[xs]);
+            } else if constexpr (JW == 32 && BBMM_TC2_SPLITLD) {
+                ptx::tmem_ld16(col, *reinterpret_cast<uint32_t(*)[16]>(sv));
             } else if constexpr (JW == 32) {
                 ptx::tmem_ld32(col, *reinterpret_cast<uint32_t(*)[32]>(sv));
             } else {
@@ -667,11 +681,15 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4], w3[JW / 4];
 #pragma unroll
             for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
+            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && MODE != 2)
+                ptx::tmem_ld16(col + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
             if (DEFER && t > 0) publish(t - 1);
+            // (the first half's stores overwrite S columns 16-19 / 24-27 of the second half)
+            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && MODE != 2) ptx::tmem_ld_wait();
             // overwrite own S columns with the A slices q0 | q1 | q2 (column maps
             // above), each half as soon as it is quantised: spreading the stores
             // over the tile measured 3 % faster than one burst at its end
-            if constexpr (JW == 32) {
+            if constexpr (JW == 32 && !(BBMM_TC2_STBURST && MODE == 3)) {
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
                 ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
@@ -679,7 +697,12 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             }
 #pragma unroll
             for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
-            if constexpr (JW == 32) {
+            if constexpr (JW == 32 && (BBMM_TC2_STBURST && MODE == 3)) {
+                ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
+                ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
+                ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));
+                if constexpr (MODE == 3) ptx::tmem_st8(col + 24, *reinterpret_cast<const uint32_t(*)[8]>(w3));
+            } else if constexpr (JW == 32) {
                 ptx::tmem_st4(col + 4, *reinterpret_cast<const uint32_t(*)[4]>(w0 + 4));
                 ptx::tmem_st4(col + 12, *reinterpret_cast<const uint32_t(*)[4]>(w1 + 4));
                 ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
