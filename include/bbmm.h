@@ -83,7 +83,7 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   §6a: ||du|| / ||u|| ~ sqrt(n) eps / sigma^2) -- D as 31-bit fixed point
  *   (per-column scale), the exponent from an fp16 hi/lo-split tensor-core
  *   distance; any t + 1 <= 33 (padded to the next instantiated column block) with
- *   d <= 30, and max |x_scaled|^2 <= 16 (precision guard).  On the fly,
+ *   any d <= 32, and max |x_scaled|^2 <= 16 (precision guard).  On the fly,
  *   Matern-5/2: distances from direct fp32 differences (the expanded form's
  *   ~1e-7 error breaks the parity bars there), 23-bit kernel
  *   values, 39-bit D; t + 1 <= 17, d <= 14.  Stored K (BBMM_STORED, t + 1 <= 33):

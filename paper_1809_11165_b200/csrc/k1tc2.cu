@@ -832,13 +832,13 @@ __global__ void k_prep_tc2(const float *__restrict__ X, int64_t n, int64_t npad,
 static int tc2_da(int d) { return ((d + 2 + 7) / 8) * 8; }
 
 // The instantiated shapes (column block C, da): RBF C in {1, 2, 4, 8} with da <= 24 and
-// {11, 17, 33} with da <= 32; Matern-5/2 C in {11, 17} with da <= 16.  Any c up to the largest
+// {11, 17, 33} with da <= 40 (every d <= kMaxDim = 32); Matern-5/2 C in {11, 17} with da <= 16.  Any c up to the largest
 // runs on the next instantiation with zero-padded columns (the padded columns add no work to the
 // MUFU-bound pair loop, only to the int8 MMAs).
 int k1tc2_cols(int kind, int d, int c) {
     const int da = tc2_da(d);
     if (kind == BBMM_MATERN52) return da > 16 ? 0 : c <= 11 ? 11 : c <= 17 ? 17 : 0;
-    if (kind != BBMM_RBF || da > 32) return 0;
+    if (kind != BBMM_RBF || da > 40) return 0;
     if (da <= 24)
         for (int v : {1, 2, 4, 8})
             if (c <= v) return v;
@@ -855,9 +855,9 @@ int k1tc2_chunks(int kind, int d, int c, int *cb) {
     *cb = big;
     return (c + big - 1) / big;
 }
-// isotropic-RBF derivative (MODE 1) instantiations: C in {11, 17, 33}, any da <= 32
+// isotropic-RBF derivative (MODE 1) instantiations: C in {11, 17, 33}, any da <= 40
 int k1tc2_deriv_cols(int d, int c) {
-    if (tc2_da(d) > 32) return 0;
+    if (tc2_da(d) > 40) return 0;
     return c <= 11 ? 11 : c <= 17 ? 17 : c <= 33 ? 33 : 0;
 }
 
@@ -944,6 +944,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
             BBMM_TC2D(11, 8) BBMM_TC2D(11, 16) BBMM_TC2D(11, 24) BBMM_TC2D(11, 32)
             BBMM_TC2D(17, 8) BBMM_TC2D(17, 16) BBMM_TC2D(17, 24) BBMM_TC2D(17, 32)
             BBMM_TC2D(33, 8) BBMM_TC2D(33, 16) BBMM_TC2D(33, 24) BBMM_TC2D(33, 32)
+            BBMM_TC2D(11, 40) BBMM_TC2D(17, 40) BBMM_TC2D(33, 40)
             throw Error{BBMM_ERR_ARG, "k1tc2: unsupported derivative shape"};
 #undef BBMM_TC2D
         }
@@ -972,6 +973,7 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         BBMM_TC2(11, 16) BBMM_TC2(17, 16) BBMM_TC2(1, 24) BBMM_TC2(2, 24) BBMM_TC2(4, 24)
         BBMM_TC2(8, 24) BBMM_TC2(11, 24) BBMM_TC2(17, 24) BBMM_TC2(11, 32) BBMM_TC2(17, 32)
         BBMM_TC2(33, 8) BBMM_TC2(33, 16) BBMM_TC2(33, 24) BBMM_TC2(33, 32)
+        BBMM_TC2(11, 40) BBMM_TC2(17, 40) BBMM_TC2(33, 40)
         throw Error{BBMM_ERR_ARG, "k1tc2: unsupported (c, d)"};
     }
 #undef BBMM_TC2
