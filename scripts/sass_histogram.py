@@ -17,7 +17,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "paper_1809_11165_b200", "build")
 KERNELS = [  # (object, mangled-name regex, label)
-    ("k1tc2.cu.o", r"k1tc2_rbfILi17ELi8ELi0ELi8E", "k1tc2_rbf<17, 8, 0> (C4 K^D)"),
+    ("k1tc2.cu.o", r"k1tc2_rbfILi17ELi8ELi3ELi8E", "k1tc2_rbf<17, 8, 3> (C4 K^D at n = 1M: 31-bit grid)"),
+    ("k1tc2.cu.o", r"k1tc2_rbfILi17ELi8ELi0ELi8E", "k1tc2_rbf<17, 8, 0> (C4 K^D, 23-bit grid)"),
     ("k1tc2.cu.o", r"k1tc2_rbfILi17ELi8ELi1ELi8E", "k1tc2_rbf<17, 8, 1> (C4 derivative)"),
     ("k1tc2.cu.o", r"k1tc2_rbfILi33ELi32ELi0ELi32E", "k1tc2_rbf<33, 32, 0> (C3 K^D)"),
     ("k1tc2.cu.o", r"k1tc2_rbfILi17ELi16ELi2ELi9E", "k1tc2_rbf<17, 16, 2, 9> (C2 Matern on the fly)"),
