@@ -246,6 +246,113 @@ k_LtR2(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
     }
 }
 
+// The same product for a tall L (K >= 128 rows: the SoR operator's Bs, m x n) with the tiles
+// streamed through a 3-stage cp.async ring instead of registers: one 256-thread block per SM,
+// each owning a contiguous row range; per 16-row step the K x 16 tile of L (row-major, rows
+// padded to 18 doubles: the 7 rows a warp reads at one kk fall in distinct banks) and the
+// 16 x c tile of R land in shared memory while the two previous steps are multiplied -- two
+// 45 KB steps in flight per SM instead of one register-staged step (k_LtR2 reached ~1.1 TB/s
+// on the 2.4 GB Bs of n = 1M, m = 300).  Thread = MPT rows of L x 4 columns of R, as k_LtR2.
+// Requires n, r0 and the rows per block even (16-byte chunks); the caller checks.
+namespace {
+__device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+}  // namespace
+constexpr int kL3T = 16, kL3Ld = 18, kL3St = 3;
+template <int MPT, int NT = 256>
+__global__ void __launch_bounds__(NT, 1)
+k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *__restrict__ R,
+       int64_t nloc, int c, int64_t rows_per_blk, double *__restrict__ part) {
+    extern __shared__ __align__(16) double sm_l3[];
+    const int stage_d = k * kL3Ld + kL3T * c + 2;      // doubles per stage (keep 16-B alignment)
+    const int stage = (stage_d + 1) & ~1;
+    const int CGN = (c + 3) / 4, MLN = NT / CGN;
+    const int g = threadIdx.x % CGN, ml = threadIdx.x / CGN;
+    const bool act = ml < MLN;
+    double acc[MPT][4];
+#pragma unroll
+    for (int j = 0; j < MPT; j++)
+#pragma unroll
+        for (int u = 0; u < 4; u++) acc[j][u] = 0.0;
+    const int64_t i_beg = (int64_t)blockIdx.x * rows_per_blk;
+    const int64_t i_end = min(nloc, i_beg + rows_per_blk);
+    const int nsteps = i_beg < i_end ? (int)((i_end - i_beg + kL3T - 1) / kL3T) : 0;
+    auto load = [&](int st) {
+        double *Ls = sm_l3 + (size_t)(st % kL3St) * stage;
+        double *Rs = Ls + (size_t)k * kL3Ld;
+        const int64_t i0 = i_beg + (int64_t)st * kL3T;
+        const int rows = (int)min((int64_t)kL3T, i_end - i0);
+        // L: k rows x 8 chunks of 2 doubles
+        for (int e = threadIdx.x; e < k * (kL3T / 2); e += NT) {
+            const int m = e >> 3, q = e & 7;
+            const bool ok = 2 * q < rows;            // rows is even except at the very end
+            const double *src = L + (int64_t)m * n + r0 + i0 + (ok ? 2 * q : 0);
+            cp16(Ls + m * kL3Ld + 2 * q, src, ok ? (2 * q + 1 < rows ? 16 : 8) : 0);
+        }
+        // R: rows x c doubles, contiguous
+        const int rd = rows * c, rchunks = (kL3T * c + 1) / 2;
+        for (int e = threadIdx.x; e < rchunks; e += NT) {
+            const int o = 2 * e;
+            const int nb = o + 1 < rd ? 16 : (o < rd ? 8 : 0);
+            cp16(Rs + o, R + i0 * c + (nb ? o : 0), nb);
+        }
+    };
+    for (int st = 0; st < kL3St - 1; st++) {
+        if (st < nsteps) load(st);
+        cp_commit();
+    }
+    for (int st = 0; st < nsteps; st++) {
+        if (st + kL3St - 1 < nsteps) load(st + kL3St - 1);
+        cp_commit();
+        cp_wait<kL3St - 1>();
+        __syncthreads();
+        const double *Ls = sm_l3 + (size_t)(st % kL3St) * stage;
+        const double *Rs = Ls + (size_t)k * kL3Ld;
+        if (act) {
+            // two kk per step: the L pair (kk, kk + 1) of a row is one 16-byte shared load
+#pragma unroll 2
+            for (int kk = 0; kk < kL3T; kk += 2) {
+                double r0[4], r1[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    r0[u] = (4 * g + u < c) ? Rs[kk * c + 4 * g + u] : 0.0;
+                    r1[u] = (4 * g + u < c) ? Rs[(kk + 1) * c + 4 * g + u] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < MPT; j++) {
+                    const int m = ml + j * MLN;
+                    const double2 l = m < k ? *reinterpret_cast<const double2 *>(Ls + m * kL3Ld + kk)
+                                            : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[j][u] = fma(l.y, r1[u], fma(l.x, r0[u], acc[j][u]));
+                }
+            }
+        }
+        __syncthreads();            // the stage is refilled by the next iteration's load
+    }
+    cp_wait<0>();
+    if (act) {
+#pragma unroll
+        for (int j = 0; j < MPT; j++) {
+            const int m = ml + j * MLN;
+            if (m < k)
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    if (4 * g + u < c) part[(int64_t)blockIdx.x * k * c + m * c + 4 * g + u] = acc[j][u];
+        }
+    }
+}
+size_t ltr3_smem(int k, int c) {
+    const int stage_d = k * kL3Ld + kL3T * c + 2;
+    return (size_t)kL3St * ((stage_d + 1) & ~1) * 8;
+}
+
 // S = C^{-1} W (k x c), C = chol factor (lower, k x k row-major).  One warp per
 // column (warp w takes columns w, w + 32, ..): forward then backward
 // substitution with the column kept in shared memory and each inner product
@@ -303,6 +410,53 @@ k_sor_expand(const double *__restrict__ Bs, int64_t n, int64_t r0, int m,
 #pragma unroll
         for (int u = 0; u < CMAX; u++)
             if (u < c) Vpart[i * cs + u] = acc[u];
+    }
+}
+
+// k_sor_expand with two rows per thread (i and i + 256 within a 512-row block slab) and T read as
+// 16-byte pairs (rows padded to an even count): half the shared-memory loads per Bs element and
+// twice the loads in flight (k_sor_expand reached ~2 TB/s on n = 1M, m = 300).
+template <int CMAX>
+__global__ void __launch_bounds__(256)
+k_sor_expand2(const double *__restrict__ Bs, int64_t n, int64_t r0, int m,
+              const double *__restrict__ T, int64_t nloc, int c, int cs, double *__restrict__ Vpart) {
+    constexpr int CP = (CMAX + 1) & ~1;
+    extern __shared__ __align__(16) double Tp[];   // m x CP (zero padded)
+    for (int e = threadIdx.x; e < m * CP; e += blockDim.x) {
+        const int a = e / CP, u = e - a * CP;
+        Tp[e] = u < c ? T[a * c + u] : 0.0;
+    }
+    __syncthreads();
+    for (int64_t base = (int64_t)blockIdx.x * 512; base < nloc; base += (int64_t)gridDim.x * 512) {
+        const int64_t i0 = base + threadIdx.x, i1 = i0 + 256;
+        const bool v0 = i0 < nloc, v1 = i1 < nloc;
+        double a0[CP], a1[CP];
+#pragma unroll
+        for (int u = 0; u < CP; u++) a0[u] = a1[u] = 0.0;
+        const double *B0 = Bs + r0 + (v0 ? i0 : 0), *B1 = Bs + r0 + (v1 ? i1 : 0);
+#pragma unroll 2
+        for (int a = 0; a < m; a++) {
+            const double b0 = v0 ? __ldg(B0 + (int64_t)a * n) : 0.0;
+            const double b1 = v1 ? __ldg(B1 + (int64_t)a * n) : 0.0;
+            const double2 *tr = reinterpret_cast<const double2 *>(Tp + a * CP);
+#pragma unroll
+            for (int u2 = 0; u2 < CP / 2; u2++) {
+                if (2 * u2 < c) {
+                    const double2 t = tr[u2];
+                    a0[2 * u2] = fma(b0, t.x, a0[2 * u2]);
+                    a0[2 * u2 + 1] = fma(b0, t.y, a0[2 * u2 + 1]);
+                    a1[2 * u2] = fma(b1, t.x, a1[2 * u2]);
+                    a1[2 * u2 + 1] = fma(b1, t.y, a1[2 * u2 + 1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CP; u++) {
+            if (u < c) {
+                if (v0) Vpart[i0 * cs + u] = a0[u];
+                if (v1) Vpart[i1 * cs + u] = a1[u];
+            }
+        }
     }
 }
 
@@ -801,6 +955,23 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
                           size_t smem_fallback) {
         const int CGN = (c + 3) / 4, MLN = 256 / CGN;
         const int need = (K + MLN - 1) / MLN;
+        // tall L (the SoR operator's Bs): the cp.async-pipelined variant
+        static const bool no_ltr3 = std::getenv("BBMM_NO_LTR3") != nullptr;
+        if (!no_ltr3 && K >= 128 && c <= 20 && need <= 16 && a.n % 2 == 0 && a.r0 % 2 == 0 &&
+            ltr3_smem(K, c) <= 200 * 1024) {
+            const int64_t rpb = ceil_div(ceil_div(std::max<int64_t>(nloc, 1), ltr_blocks), kL3T) * kL3T;
+            static DeviceOnce attr3;
+            attr3(ctx->device, [] {
+                for (auto f : {k_LtR3<4>, k_LtR3<8>, k_LtR3<12>, k_LtR3<16>})
+                    BBMM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   200 * 1024));
+            });
+            // (512-thread blocks with half the rows per thread measured slower: 1.40 vs 1.15 ms)
+            auto f = need <= 4 ? k_LtR3<4> : need <= 8 ? k_LtR3<8> : need <= 12 ? k_LtR3<12>
+                                                                               : k_LtR3<16>;
+            f<<<ltr_blocks, 256, ltr3_smem(K, c), sm>>>(Lp, a.n, a.r0, K, Rp, nloc, c, rpb, part_out);
+            return;
+        }
         if (c <= 20 && need <= 16) {
             const int KT = K <= 256 ? 32 : 16;
             const int64_t rpb = ceil_div(ceil_div(std::max<int64_t>(nloc, 1), ltr_blocks), KT) * KT;
@@ -853,9 +1024,19 @@ void mbcg_run(bbmm_ctx_s *ctx, const MbcgArgs &a, const double *B, int64_t ldb,
         }
         if (multi) allreduce_sum(ctx, Tsor, (size_t)msor * c);
         if (nloc > 0) {
-            const int eg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 4 * kNumSMs));
-            sor_expand<<<eg, 256, (size_t)msor * c * 8, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc, c,
-                                                             cs, Vpart);
+            static const bool no_sor2 = std::getenv("BBMM_NO_SOR2") != nullptr;
+            const size_t sm2 = (size_t)msor * (c <= 8 ? 8 : 18) * 8;   // m x CP of the instantiation
+            if (!no_sor2 && c <= 17 && sm2 <= 48 * 1024) {
+                const int eg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 512), 4 * kNumSMs));
+                if (c <= 8)
+                    k_sor_expand2<8><<<eg, 256, sm2, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc, c, cs, Vpart);
+                else
+                    k_sor_expand2<17><<<eg, 256, sm2, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc, c, cs, Vpart);
+            } else {
+                const int eg = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nloc, 256), 4 * kNumSMs));
+                sor_expand<<<eg, 256, (size_t)msor * c * 8, sm>>>(a.sor_B, a.n, a.r0, msor, Tsor, nloc, c,
+                                                                 cs, Vpart);
+            }
             launches++;
         }
         if (e1) record_event(ctx, e1);
