@@ -12,11 +12,13 @@ for r in rows[hi + 1:]:
     if len(r) < len(hdr) or r[idx['Metric Name']] != 'gpu__time_duration.sum':
         continue
     full = r[idx['Kernel Name']]
-    base = full.replace('void ', '', 1).replace('<unnamed>::', '')
+    base = full.replace('void ', '', 1)
+    for pre in ('<unnamed>::', 'unnamed>::', '(anonymous namespace)::'):
+        base = base.replace(pre, '')
     m = re.match(r'([\w:]+)', base)
     name = m.group(1) if m else full
     tmpl = re.search(r'<([^>]*)>', full)
-    if tmpl and ('k1' in name or 'k2' in name or 'k7' in name):
+    if tmpl and ('k1' in name or 'k2' in name or 'k7' in name or 'LtR' in name or 'expand' in name):
         name += '<' + tmpl.group(1) + '>'
     tot[name] += float(r[idx['Metric Value']].replace(',', '')) * scale[r[idx['Metric Unit']]]
     cnt[name] += 1
