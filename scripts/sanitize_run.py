@@ -5,7 +5,9 @@
 C0 (fused mBCG, CUDA-core operator), C4-shaped n = 3000 (K1-TC, per-step kernels + the captured
 graph), C1 stored K (K2-TC), C2-shaped Matern on the fly (K1-TC MODE 2) and its tensor-core
 derivative pass, C3-shaped n = 20 000 (K1-TC <33>, the RBF-ARD tensor-core derivative pass),
-predictions and the SoR operator.  Prints one line per call."""
+predictions and the SoR operator (both skinny-product kernels), the 31-bit-grid K1-TC (MODE 3) and
+the 23-bit one over more than one uint32 drain window, and K1-TC column chunks.  Prints one line
+per call."""
 import os
 import sys
 
@@ -44,6 +46,11 @@ run("C4", 3000, env={"BBMM_NO_FUSED_MBCG": "1"})            # per-step kernels, 
 run("C1", 3338)                                             # stored K2-TC
 run("C2", 3000, kmode=bb.ONTHEFLY, env={"BBMM_DERIV_TC_MIN_N": "0"})   # Matern MODE 2 + deriv_tc
 run("C3", 20000, p=4)                                       # K1-TC <33>, deriv_tc2
+ctx.set_matmul_precision(bb.INT8EXACT31)
+run("C4", 30000, p=2, t=16, k=10)                           # K1-TC MODE 3: > 1 drain window
+ctx.set_matmul_precision(bb.INT8EXACT)
+run("C4", 30000, p=2, t=16, k=10)                           # K1-TC MODE 0: > 1 drain window
+run("C4", 1500, t=40, k=10)                                 # column chunks (2 x 33) + MODE-1 chunks
 cfg, pr, X, y, h = run("C4", 2000, t=5, k=10)
 Xs = torch.from_numpy(synth.test_points(cfg, 20)).cuda()
 mean, var = bb.predict(ctx, X, y, Xs, h, k=10, max_iter=10)
@@ -52,6 +59,9 @@ Xu = torch.from_numpy(pr.X[:100].copy()).cuda()
 B = torch.from_numpy(synth.random_block(cfg.n, 4, seed=1).astype(np.float64)).cuda()
 r = bb.sor_mbcg(ctx, X, Xu, h, B, k=5, max_iter=10)
 print("sor", float(r["relres"][0]))
+Xu2 = torch.from_numpy(pr.X[:200].copy()).cuda()              # m >= 128: the cp.async k_LtR3 path
+r = bb.sor_mbcg(ctx, X, Xu2, h, B, k=5, max_iter=10)
+print("sor m=200", float(r["relres"][0]))
 torch.cuda.synchronize()
 ctx.close()
 print("sanitize run done")
