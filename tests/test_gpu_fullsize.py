@@ -4,7 +4,8 @@ The cache is written by scripts/make_oracle_cache.py, which calls only oracle/ a
 oracle at these sizes costs minutes to an hour of host time, so it is not recomputed per run).
 Each file carries a SHA-256 of its inputs; the test rebuilds X, y, theta with synth and refuses a
 stale cache.  Sizes (VERDICT r1 "next" 1): C4 shape n = 131 072 (4.5 uint32 drain windows of the
-on-the-fly tcgen05 kernel, per-step mBCG kernels, the MODE-1 derivative over many windows), C3
+on-the-fly tcgen05 kernel, per-step mBCG kernels, the MODE-1 derivative over many windows) and
+n = 262 144 (where the default operator switches to the 31-bit kernel-value grid), C3
 shape n = 80 000 (ARD, t = 32, tensor-core derivative pass), C2 at its full BASELINE size
 n = 45 730 (stored K, Matern-5/2 ARD).
 
@@ -35,7 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LARGE = os.path.join(HERE, "golden", "large")
 OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
 
-CASES = [("C4", 131072), ("C3", 80000), ("C2", 45730)]
+CASES = [("C4", 131072), ("C4", 262144), ("C3", 80000), ("C2", 45730)]
 # Regime B: the solve bar is twice the oracle's own rounding floor -- how far the
 # fp64 oracle's solves move when its right-hand side moves by one ulp (<name>_n<n>_floor.json,
 # scripts/oracle_rounding_floor.py) -- and at least the north-star 1e-4; the gradient bar is 5x the
