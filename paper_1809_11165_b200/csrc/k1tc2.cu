@@ -548,7 +548,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 // k~ r^2 <= 2/e ~= 0.74): the 2^-23 grid step is 1.39x coarser relative to
                 // the derivative value (about half a bit), measured inside the gradient bar
                 // (MODE 1 margin)
-                if (MODE == 1) kv *= fmaxf(-sj, 0.0f);
+                // (one FMUL.SAT: the [0, 1] saturation clamps the rounding-positive S near the
+                //  diagonal to 0 like max(-S, 0) did, and never binds above: k~ (-S) <= 0.53)
+                if (MODE == 1) kv = __saturatef(kv * -sj);
                 q[v] = __float_as_uint(kv);
             }
             if constexpr (MODE == 3 && BBMM_TC2_ABL != 3) {
