@@ -86,6 +86,7 @@ CASES = [  # name, n, kmode, prec, nranks, expected matmul path
     ("C3", 2000, bb.ONTHEFLY, bb.INT8EXACT, 2, 2),
     ("C4", 3000, bb.ONTHEFLY, bb.FP64ACC, 2, 0),
     ("C4", 300, bb.ONTHEFLY, bb.INT8EXACT, 4, 2),     # n = 300, nb = 128: rank 3 owns no rows
+    ("C4", 3000, bb.ONTHEFLY, bb.INT8EXACT31, 3, 2),  # the 31-bit k~ grid (K1-TC MODE 3)
 ]
 
 
