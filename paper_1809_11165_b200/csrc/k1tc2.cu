@@ -528,20 +528,31 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     asm("mov.b64 {%0, %1}, %2;" : "=r"(sw[v]), "=r"(sw[v + 1]) : "l"(ps));
                 }
             }
+            if constexpr (MODE == 2) {
+                // sv holds +rh'^2 with rh' = log2(e) rh (a sum of squares: no clamp);
+                // k~ = (1 + rh + rh^2/3) 2^(-rh') with rh = ln2 rh'; the polynomial and the
+                // product for two points per FFMA2 / FMUL2
+#pragma unroll
+                for (int v = 0; v < 4; v += 2) {
+                    const float rh0 = sqrt_approx(__uint_as_float(sw[v]));
+                    const float rh1 = sqrt_approx(__uint_as_float(sw[v + 1]));
+                    const float e0 = ex2_approx(-rh0), e1 = ex2_approx(-rh1);
+                    unsigned long long prh, prs, pe, pp;
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(prh) : "f"(rh0), "f"(rh1));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(prs) : "r"(sw[v]), "r"(sw[v + 1]));
+                    asm("mov.b64 %0, {%1, %2};" : "=l"(pe) : "f"(e0), "f"(e1));
+                    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(prh), "l"(0x3F3172183F317218ull),
+                        "l"(0x3F8000003F800000ull));                         // 1 + ln2 rh'
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(pp) : "l"(prs), "l"(0x3E23FEA03E23FEA0ull));
+                    asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(pp) : "l"(pe));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pp));
+                }
+            }
+            if constexpr (MODE != 2) {
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float sj = __uint_as_float(sw[v]);
-                float kv;
-                if (MODE == 2) {
-                    // sv holds +rh'^2 with rh' = log2(e) rh (a sum of squares: no clamp);
-                    // k~ = (1 + rh + rh^2/3) 2^(-rh') with rh = ln2 rh'
-                    const float rs2 = sj;
-                    const float rh = sqrt_approx(rs2);
-                    kv = fmaf(rs2, 0.16015100463940046f /* ln2^2 / 3 */,
-                              fmaf(rh, 0.69314718055994531f, 1.0f)) * ex2_approx(-rh);
-                } else {
-                    kv = ex2_approx(sj);
-                }
+                float kv = ex2_approx(sj);
                 // r^2 = -2 ln2 S (S = -(log2 e / 2) r^2), clamped at 0 (S may be
                 // +eps by rounding near the diagonal).  The factor 2 ln 2 is applied in the
                 // epilogue, so the quantised value is k~ (-S) <= 1/(e ln 2)/2 ~= 0.53 (not
@@ -552,6 +563,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 //  diagonal to 0 like max(-S, 0) did, and never binds above: k~ (-S) <= 0.53)
                 if (MODE == 1) kv = __saturatef(kv * -sj);
                 q[v] = __float_as_uint(kv);
+            }
             }
             if constexpr (MODE == 3 && BBMM_TC2_ABL != 3) {
                 // 31-bit grid: the fixed-point value F = k~ 2^31 (exact for k~ >= 2^-8, where the
@@ -663,11 +675,10 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                             }
                         }
                     }
-                    float a0, a1, b0, b1;
-                    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc2[0]));
-                    asm("mov.b64 {%0, %1}, %2;" : "=f"(b0), "=f"(b1) : "l"(acc2[1]));
-                    sv[2 * jp] = __float_as_uint(a0 + b0);
-                    sv[2 * jp + 1] = __float_as_uint(a1 + b1);
+                    // the two partial sums of the pair, added in one FADD2
+                    unsigned long long ssum;
+                    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(ssum) : "l"(acc2[0]), "l"(acc2[1]));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(sv[2 * jp]), "=r"(sv[2 * jp + 1]) : "l"(ssum));
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&free_x[xs]);
