@@ -120,3 +120,17 @@ def test_default_grid_follows_the_error_model(ctx, n, bits):
     finally:
         ctx.set_matmul_precision(bb.INT8EXACT)
     assert g["stats"]["kgrid_bits"] == 23
+
+
+def test_default_grid_with_column_chunks_sampled_rows(ctx, orc):
+    """n = 300 000 (the default operator on the 31-bit grid) with 41 columns (two column chunks of
+    33): sampled rows vs the oracle at the element-wise bound."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 300000)
+    pr = synth.make_problem(cfg, seed=0)
+    D = synth.random_block(cfg.n, 41, seed=4).astype(np.float64)
+    V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr)).cpu().numpy()
+    rows = np.unique(np.concatenate([[0, cfg.n - 1], np.random.default_rng(1).integers(0, cfg.n, 30)]))
+    ref = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D, rows=rows)
+    absb = orc.kernel_matmul(cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, np.abs(D), rows=rows)
+    err = np.abs(V[rows] - ref)
+    assert np.all(err <= 2e-6 * absb + 1e-12), float((err / absb).max())
