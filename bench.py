@@ -51,6 +51,10 @@ DTYPE = {
     3: "stored 30-bit fixed-point K (4 u8 slices, fp64-built) x 55-bit fixed-point D (7 u8 slices), "
        "exact int32 accumulation on tcgen05; fp64 CG",
 }
+DTYPE31M = ("31-bit fixed-point k~ (4 u8 slices: the fp32 Matern-5/2 value exactly, from fp32 direct "
+            "distances and MUFU sqrt + ex2) x 55-bit fixed-point D (7 u8 slices), exact int32 "
+            "accumulation of the slice products on tcgen05 (those below 2^-52 of the scale dropped); "
+            "fp64 CG")
 DTYPE31 = ("31-bit fixed-point k~ (4 u8 slices: the fp32 MUFU ex2 value exactly, of an fp16-split "
            "tensor-core exponent) x 31-bit fixed-point D (4 u8 slices), exact int32 accumulation of "
            "the slice products on tcgen05 (those below 2^-38 of the scale dropped); fp64 CG")
@@ -79,10 +83,10 @@ def tensor_frac(cfg, world, mm_ms, pk, detail=False, kgrid=23):
         nb = 4 * blk
         kdist = 32 if da == 8 else 3 * r16(da)
         nsum = 2 * nb + min(nb, r16(3 * blk)) + (r16(2 * blk) if kgrid == 31 else 0)
-    else:                                           # Matern: five D slices, BLK = round16
-        nb = 5 * r16(c1)
+    else:               # Matern: BLK = round16; five D slices x 3 k~ slices, or 7 x 4 (31-bit grid)
+        blk = r16(c1)
         kdist = 0
-        nsum = 3 * nb
+        nsum = 15 * blk if kgrid != 31 else (7 + 6 + 5 + 4) * blk
     rows = -(-(-(-cfg.n // world)) // 128) * 128
     cols = -(-cfg.n // 128) * 128
     f16 = 2.0 * rows * cols * kdist
@@ -344,7 +348,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "s_per_mll_grad": ms / 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": DTYPE[path] if not (path == 2 and stats[-1].get("kgrid_bits") == 31) else DTYPE31,
+        "dtype": (DTYPE[path] if not (path == 2 and stats[-1].get("kgrid_bits") == 31)
+                  else DTYPE31M if cfg.kind != synth.RBF else DTYPE31),
         "data": "synthetic (seeded; SURVEY.md §8d recipe)",
         "config": {"workload": f"{cfg.name}: exact GP MLL+grad, "
                                f"{'RBF' if cfg.kind == 0 else 'Matern-5/2'}"

@@ -123,6 +123,9 @@ static_assert((double)WINDOW * 162690.0 < 4294967296.0, "uint32 window bound");
 // becomes block 3's q2 p0 + q1 p1 + q0 p2 + r p3 <= 128*255 + 2*255*255 + 255*128 = 195330
 constexpr int WINDOW31 = (int)(4294967295ull / 195330ull) / BK * BK;
 static_assert((double)WINDOW31 * 195330.0 < 4294967296.0, "uint32 window bound (MODE 3)");
+// MODE 4 (Matern, four k~ slices x seven D slices): at most four products of <= 255^2 per block
+constexpr int WINDOW4 = (int)(4294967295ull / 260100ull) / BK * BK;
+static_assert((double)WINDOW4 * 260100.0 < 4294967296.0, "uint32 window bound (MODE 4)");
 constexpr int kThreads = 32 * (NCW + 2);
 constexpr int PRODUCER_WARP = NCW, MMA_WARP = NCW + 1;
 static_assert(NCW * JW == 4 * BK, "4 lane quarters x BK columns");
@@ -150,11 +153,13 @@ template <int C, int DA, int ND = 4>
 struct Cfg {
     static constexpr int C1 = C + 1;
     static_assert(C1 <= 48, "too many columns");
-    static_assert(ND == 4 || ND == 5, "D slices");
+    static_assert(ND == 4 || ND == 5 || ND == 7, "D slices");
     static constexpr int BLK = ND == 4 ? (C1 + 3) & ~3 : (C1 + 15) & ~15;
     static constexpr int NB = ND * BLK;                        // D-slice rows (MMA N)
     static_assert(NB % 16 == 0 && NB <= 256, "MMA N");
-    static constexpr int NBLK = ND + 2;                        // accumulator blocks
+    // accumulator blocks: ND + 2 (three k~ slices); ND = 7 (MODE 4: four k~ slices x 55-bit D)
+    // keeps the 7 blocks of weight 2^64 .. 2^16 (the dropped products are < 2^-52 of the scale)
+    static constexpr int NBLK = ND == 7 ? 7 : ND + 2;
     static constexpr int ACC_COLS = NBLK * BLK;
     static constexpr int ACC_END = r32(ACC_COLS);
     static constexpr int NBUF_FIT = (512 - ACC_END) / BK;
@@ -208,8 +213,9 @@ struct Cfg {
 // the stores).
 template <int C, int BLK, int ACC_END, int ND>
 __device__ __noinline__ void drain_window(uint32_t lane_base, double (*acc_sm)[BM], int rl, int h) {
-    constexpr int NBLK = ND + 2;
-    constexpr double W0 = ND == 4 ? 0x1p40 : 0x1p48;    // weight of block 0: 2^(8 (ND + 1))
+    constexpr int NBLK = ND == 7 ? 7 : ND + 2;
+    // weight of block 0: q2 (2^16 in k~ 2^23 units) times the top D slice (2^(8 (ND - 1)))
+    constexpr double W0 = ND == 4 ? 0x1p40 : ND == 5 ? 0x1p48 : 0x1p64;
     constexpr uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     constexpr int M = (C + NPS) / NPS;             // columns cc = h + NPS m <= C per warp
     uint32_t v[M][NBLK];
@@ -255,7 +261,9 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
           const uint8_t *__restrict__ Bpack, const double *__restrict__ Sc, int64_t r0,
           int64_t nloc, int64_t tiles_per_split, int64_t ntiles, double s,
           double *__restrict__ Vpart, int ldv, int coff) {
-    constexpr int ND = MODE == 2 ? 5 : 4;
+    constexpr bool MAT = MODE == 2 || MODE == 4;     // Matern: direct distances, no distance MMA
+    constexpr bool G31 = MODE == 3 || MODE == 4;     // k~ on the 31-bit grid (four A slices)
+    constexpr int ND = MODE == 2 ? 5 : MODE == 4 ? 7 : 4;
     using K = Cfg<C, DA, ND>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -270,13 +278,13 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     const int warp = tid >> 5, lane = tid & 31;
     const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
     const int ntl = (int)(min(ntiles, t0 + tiles_per_split) - t0);
-    constexpr int TPW = (MODE == 3 ? WINDOW31 : WINDOW) / BK;
+    constexpr int TPW = (MODE == 4 ? WINDOW4 : MODE == 3 ? WINDOW31 : WINDOW) / BK;
 
     if (tid == 0) {
         for (int q = 0; q < K::XS; q++) {
             ptx::mbar_init(&full_x[q], 1);
             // MODE 2 reads the x tile on the compute warps (direct distances), not in an MMA
-            ptx::mbar_init(&free_x[q], MODE == 2 ? NCW : 1);
+            ptx::mbar_init(&free_x[q], MAT ? NCW : 1);
         }
         for (int q = 0; q < K::QS; q++) {
             ptx::mbar_init(&full_q[q], 1);
@@ -332,14 +340,16 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         // cannot overwrite it early: no buffer-free round trip is needed.
         constexpr uint32_t IDS = K::H16 ? ptx::idesc_f16(BM, BK) : ptx::idesc_tf32(BM, BK);
         constexpr uint32_t IDQ = ptx::idesc_i8(BM, K::NB, false, false);
-        constexpr uint32_t IDQ1 = ptx::idesc_i8(BM, K::N1, false, false);
-        constexpr uint32_t IDQ0 = ptx::idesc_i8(BM, K::N0, false, false);
+        // MODE 4 (ND = 7, blocks of weight 2^64 .. 2^16): q2 x [p6..p0], q1 x [p6..p1],
+        // q0 x [p6..p2], r x [p6..p3] -- N = 7, 6, 5, 4 BLK, every product of the kept weights
+        constexpr uint32_t IDQ1 = ptx::idesc_i8(BM, ND == 7 ? 6 * K::BLK : K::N1, false, false);
+        constexpr uint32_t IDQ0 = ptx::idesc_i8(BM, ND == 7 ? 5 * K::BLK : K::N0, false, false);
         // MODE 3 residual slice r x [p3 p2 (p1)]: N = round16(2 BLK) -- the extra columns land
         // in blocks of their own weight (r p1 -> block 5) or, at BLK = 4, in the padding
         // column block 6 that is never drained (ACC_END >= 7 BLK there)
         constexpr int NR = r16(2 * K::BLK);   // (r x p3 alone, N = round16(BLK): no faster)
         static_assert(MODE != 3 || NR <= 3 * K::BLK || 7 * K::BLK <= K::ACC_END, "residual N");
-        constexpr uint32_t IDQR = ptx::idesc_i8(BM, NR, false, false);
+        constexpr uint32_t IDQR = ptx::idesc_i8(BM, ND == 7 ? 4 * K::BLK : NR, false, false);
         const bool leader = ptx::elect_one();
         ptx::mbar_wait(&init_done, 0);
         ptx::tc_fence_after();
@@ -353,7 +363,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             const int xi = t % K::XS;
             const int b = t % K::NBUF;
             ptx::tc_fence_after();
-            if (MODE == 2) {
+            if (MAT) {
                 // no distance MMA: only signal that buffer b is free again once the int8
                 // MMAs issued so far (the last readers of b) have completed
                 if (leader) ptx::mma_commit(&s_full[b]);
@@ -391,7 +401,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             __syncwarp();
         };
         for (int t = 0; t < K::NBUF && t < ntl; t++) {
-            if (MODE != 2) wait_x(t);
+            if (!MAT) wait_x(t);
             issue_dist(t);
         }
         for (int t = 0; t < ntl; t++) {
@@ -401,7 +411,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             const bool first = (t % TPW) == 0;
             // operands of the next distance MMA: normally resident long ago, so
             // this check overlaps the wait for the compute warps below
-            if (MODE != 2 && t + K::NBUF < ntl) wait_x(t + K::NBUF);
+            if (!MAT && t + K::NBUF < ntl) wait_x(t + K::NBUF);
             if (first && win > 0) ptx::mbar_wait(&acc_empty, (uint32_t)((win - 1) & 1));
             ptx::mbar_wait(&a_full[b], (uint32_t)((t / K::NBUF) & 1));
             ptx::mbar_wait(&full_q[qi], (uint32_t)((t / K::QS) & 1));
@@ -415,7 +425,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     ptx::mma_i8_ts(tmem + 0, aq + 32 * ks + 16, bd, IDQ, 1u);              // q2
                     ptx::mma_i8_ts(tmem + K::BLK, aq + 32 * ks + 8, bd, IDQ1, 1u);         // q1
                     ptx::mma_i8_ts(tmem + 2 * K::BLK, aq + 32 * ks + 0, bd, IDQ0, 1u);     // q0
-                    if constexpr (MODE == 3 && BBMM_TC2_ABL != 1)
+                    if constexpr (G31 && BBMM_TC2_ABL != 1)
                         ptx::mma_i8_ts(tmem + 3 * K::BLK, aq + 32 * ks + 24, bd, IDQR, 1u);  // r
                 }
                 ptx::mma_commit(&free_q[qi]);
@@ -430,8 +440,8 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
         const int64_t row = (int64_t)blockIdx.x * BM + sub * 32 + lane;
         const bool valid = row < nloc;
         // MODE 2: this row's scaled inputs (plain layout of its XB tile)
-        float xrow[MODE == 2 ? DM : 1];
-        if constexpr (MODE == 2) {
+        float xrow[MAT ? DM : 1];
+        if constexpr (MAT) {
             const int64_t rg = r0 + row;
             const int jr = (int)(rg % BK);
             const float *src = XB + (rg / BK) * (int64_t)(2 * DA * BK) + (jr >> 1) * (2 * DA) + (jr & 1);
@@ -528,7 +538,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     asm("mov.b64 {%0, %1}, %2;" : "=r"(sw[v]), "=r"(sw[v + 1]) : "l"(ps));
                 }
             }
-            if constexpr (MODE == 2) {
+            if constexpr (MAT) {
                 // sv holds +rh'^2 with rh' = log2(e) rh (a sum of squares: no clamp);
                 // k~ = (1 + rh + rh^2/3) 2^(-rh') with rh = ln2 rh'; the polynomial and the
                 // product for two points per FFMA2 / FMUL2
@@ -548,7 +558,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                     asm("mov.b64 {%0, %1}, %2;" : "=r"(q[v]), "=r"(q[v + 1]) : "l"(pp));
                 }
             }
-            if constexpr (MODE != 2) {
+            if constexpr (!MAT) {
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float sj = __uint_as_float(sw[v]);
@@ -565,7 +575,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
                 q[v] = __float_as_uint(kv);
             }
             }
-            if constexpr (MODE == 3 && BBMM_TC2_ABL != 3) {
+            if constexpr (G31 && BBMM_TC2_ABL != 3) {
                 // 31-bit grid: the fixed-point value F = k~ 2^31 (exact for k~ >= 2^-8, where the
                 // fp32 k~ has no bits below 2^-31; floor below) as two 16-bit halves, F = H 2^16 + L:
                 //   h = rz(2^15 k~ + 2^23)              = 2^23 + H,  H = floor(2^15 k~) <= 2^15
@@ -645,7 +655,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             ptx::tc_fence_after();
             uint32_t sv[JW];
             const uint32_t col = my_col + b * BK;
-            if constexpr (MODE == 2) {
+            if constexpr (MAT) {
                 // S = -r^2 from direct differences with the tile's x_j (broadcast loads)
                 const int xs = t % K::XS;
                 ptx::mbar_wait(&full_x[xs], (uint32_t)((t / K::XS) & 1));
@@ -690,36 +700,36 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
 #pragma unroll
                 for (int u = 0; u < 4; u++) ptx::tmem_ld4(col + 8 * u, sv + 4 * u);
             }
-            if constexpr (MODE != 2) ptx::tmem_ld_wait();
+            if constexpr (!MAT) ptx::tmem_ld_wait();
             uint32_t w0[JW / 4], w1[JW / 4], w2[JW / 4], w3[JW / 4];
 #pragma unroll
             for (int u = 0; u < JW / 8; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
-            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && MODE != 2)
+            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && !MAT)
                 ptx::tmem_ld16(col + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
             if (DEFER && t > 0) publish(t - 1);
             // (the first half's stores overwrite S columns 16-19 / 24-27 of the second half)
-            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && MODE != 2) ptx::tmem_ld_wait();
+            if constexpr (JW == 32 && BBMM_TC2_SPLITLD && !MAT) ptx::tmem_ld_wait();
             // overwrite own S columns with the A slices q0 | q1 | q2 (column maps
             // above), each half as soon as it is quantised: spreading the stores
             // over the tile measured 3 % faster than one burst at its end
-            if constexpr (JW == 32 && !(BBMM_TC2_STBURST && MODE == 3)) {
+            if constexpr (JW == 32 && !(BBMM_TC2_STBURST && G31)) {
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
                 ptx::tmem_st4(col + 16, *reinterpret_cast<const uint32_t(*)[4]>(w2));
-                if constexpr (MODE == 3 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 24, *reinterpret_cast<const uint32_t(*)[4]>(w3));
+                if constexpr (G31 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 24, *reinterpret_cast<const uint32_t(*)[4]>(w3));
             }
 #pragma unroll
             for (int u = JW / 8; u < JW / 4; u++) quant4(sv, u, w0[u], w1[u], w2[u], w3[u]);
-            if constexpr (JW == 32 && (BBMM_TC2_STBURST && MODE == 3)) {
+            if constexpr (JW == 32 && (BBMM_TC2_STBURST && G31)) {
                 ptx::tmem_st8(col + 0, *reinterpret_cast<const uint32_t(*)[8]>(w0));
                 ptx::tmem_st8(col + 8, *reinterpret_cast<const uint32_t(*)[8]>(w1));
                 ptx::tmem_st8(col + 16, *reinterpret_cast<const uint32_t(*)[8]>(w2));
-                if constexpr (MODE == 3) ptx::tmem_st8(col + 24, *reinterpret_cast<const uint32_t(*)[8]>(w3));
+                if constexpr (G31) ptx::tmem_st8(col + 24, *reinterpret_cast<const uint32_t(*)[8]>(w3));
             } else if constexpr (JW == 32) {
                 ptx::tmem_st4(col + 4, *reinterpret_cast<const uint32_t(*)[4]>(w0 + 4));
                 ptx::tmem_st4(col + 12, *reinterpret_cast<const uint32_t(*)[4]>(w1 + 4));
                 ptx::tmem_st4(col + 20, *reinterpret_cast<const uint32_t(*)[4]>(w2 + 4));
-                if constexpr (MODE == 3 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 28, *reinterpret_cast<const uint32_t(*)[4]>(w3 + 4));
+                if constexpr (G31 && BBMM_TC2_ABL != 2) ptx::tmem_st4(col + 28, *reinterpret_cast<const uint32_t(*)[4]>(w3 + 4));
             } else {
                 ptx::tmem_st4(col + 0, *reinterpret_cast<const uint32_t(*)[4]>(w0));
                 ptx::tmem_st4(col + 8, *reinterpret_cast<const uint32_t(*)[4]>(w1));
@@ -733,7 +743,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
             double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * ldv + coff;
-            const double base = s * (ND == 4 ? 0x1p-53 : 0x1p-61) *
+            const double base = s * (ND == 4 ? 0x1p-53 : ND == 5 ? 0x1p-61 : 0x1p-77) *
                                 (MODE == 1 ? 1.3862943611198906 : 1.0);   // MODE 1: r^2 = -2 ln2 S
             const double cacc = acc_sm[C][rl];
 #pragma unroll
@@ -908,7 +918,7 @@ template <int C, int DA, int MODE, int DM = DA>
 static int launch_tc2(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_t *Bp,
                       const double *S, int64_t n, int64_t r0, int64_t nloc, double s,
                       double *Vpart, size_t cap, int ldv, int coff) {
-    using K = tc2::Cfg<C, DA, MODE == 2 ? 5 : 4>;
+    using K = tc2::Cfg<C, DA, MODE == 2 ? 5 : MODE == 4 ? 7 : 4>;
     const int64_t ntiles = ceil_div(n, tc2::BK);
     const int64_t rb = ceil_div(nloc, tc2::BM);
     int64_t sp = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, rb), ntiles));
@@ -964,15 +974,19 @@ int k1tc2_matmul(bbmm_ctx_s *ctx, const float *Xa, const float *XB, const uint8_
         if (ev1) record_event(ctx, ev1);
         return sp;
     }
-    if (mode == 2) {   // Matern-5/2
+    if (mode == 2 || mode == 4) {   // Matern-5/2: 23-bit grid, 39-bit D / 31-bit grid, 55-bit D
+#define BBMM_TC2M(CC, DD, DMM) \
+    (mode == 4 ? launch_tc2<CC, DD, 4, DMM>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff) \
+               : launch_tc2<CC, DD, 2, DMM>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff))
         if (nloc > 0) {
-            if (c == 17 && d == 9) sp = launch_tc2<17, 16, 2, 9>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
-            else if (c == 17 && da == 16) sp = launch_tc2<17, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
-            else if (c == 17 && da == 8) sp = launch_tc2<17, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
-            else if (c == 11 && da == 16) sp = launch_tc2<11, 16, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
-            else if (c == 11 && da == 8) sp = launch_tc2<11, 8, 2>(ctx, Xa, XB, Bp, S, n, r0, nloc, s, Vpart, cap, ldv, coff);
+            if (c == 17 && d == 9) sp = BBMM_TC2M(17, 16, 9);
+            else if (c == 17 && da == 16) sp = BBMM_TC2M(17, 16, 16);
+            else if (c == 17 && da == 8) sp = BBMM_TC2M(17, 8, 8);
+            else if (c == 11 && da == 16) sp = BBMM_TC2M(11, 16, 16);
+            else if (c == 11 && da == 8) sp = BBMM_TC2M(11, 8, 8);
             else throw Error{BBMM_ERR_ARG, "k1tc2: unsupported Matern shape"};
         }
+#undef BBMM_TC2M
         if (ev1) record_event(ctx, ev1);
         return sp;
     }
@@ -1014,7 +1028,6 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         if (h.kind == BBMM_RBF && !(max_sq <= 16.0f)) return op;
         op.version = 2;
         op.kind = h.kind;
-        op.nd = h.kind == BBMM_MATERN52 ? 5 : 4;
         op.cb = nch > 0 ? cbk : k1tc2_cols(h.kind, d, c);
         op.nch = nch > 0 ? nch : 1;
         op.npad = npad;
@@ -1022,9 +1035,16 @@ TcOperand tc_prepare(bbmm_ctx_s *ctx, const float *X, int64_t n, int d, int c, c
         // MUFU's 2.8e-8 random part plus the grid's 4.2e-8) moves the solves by about
         // sqrt(n) eps s / sigma^2; where that would pass 0.8e-4 (a 20 % margin under the 1e-4
         // bar) the 31-bit grid (MUFU error only, 3.3e-8) is used -- C4 at n = 1M: 1.77e-4 -> 31 bits
+        // Matern-5/2 on the fly keeps the 31-bit grid (with 55-bit D, MODE 4) unless the 23-bit
+        // grid is forced: most of its kernel values are small (k~ ~ e^-rh), where the 23-bit
+        // grid's ABSOLUTE 2^-24 error is large relative to the fp32 value, and the C2 shape is not
+        // converged at p -- full C2 on the 23-bit grid with 39-bit D (MODE 2) missed the regime-B
+        // bars (solve 3.2e-3 vs the fp64 oracle; the fp32-valued FP64ACC operator: 4.1e-4)
         const double est23 = std::sqrt((double)n) * 5.3e-8 * h.s / h.noise_var;
-        op.grid31 = h.kind == BBMM_RBF &&
-                    (ctx->matmul_grid == 31 || (ctx->matmul_grid == 0 && est23 > 0.8e-4));
+        op.grid31 = h.kind == BBMM_RBF
+                        ? (ctx->matmul_grid == 31 || (ctx->matmul_grid == 0 && est23 > 0.8e-4))
+                        : ctx->matmul_grid != 23;
+        op.nd = h.kind == BBMM_MATERN52 ? (op.grid31 ? 7 : 5) : 4;
         op.Xa = xa;
         op.XB = xb;
     }
@@ -1060,7 +1080,7 @@ int tc_matmul(bbmm_ctx_s *ctx, const TcOperand &op, const uint8_t *Bp, const dou
     }
     if (op.kind == BBMM_MATERN52) {
         BBMM_REQUIRE(mode == 0, "k1tc2: no Matern derivative mode");
-        mode = 2;
+        mode = op.grid31 ? 4 : 2;
     }
     if (mode == 0 && op.grid31) mode = 3;   // the blackbox matmul on the 31-bit k~ grid
     if (op.nch > 1 && c == op.cb) {      // column chunks (tc_pack layout; mbcg and derivative)

@@ -36,7 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LARGE = os.path.join(HERE, "golden", "large")
 OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
 
-CASES = [("C4", 131072), ("C4", 262144), ("C3", 80000), ("C2", 45730)]
+CASES = [("C4", 131072), ("C4", 262144), ("C3", 80000), ("C3", 131072), ("C2", 45730)]
 # Regime B: the solve bar is twice the oracle's own rounding floor -- how far the
 # fp64 oracle's solves move when its right-hand side moves by one ulp (<name>_n<n>_floor.json,
 # scripts/oracle_rounding_floor.py) -- and at least the north-star 1e-4; the gradient bar is 5x the
@@ -75,7 +75,7 @@ def ctx():
     c.close()
 
 
-def _run(ctx, name, n, prec):
+def _run(ctx, name, n, prec, kmode=None):
     meta, z = _load(name, n)
     cfg = synth.scaled(synth.CONFIGS[name], n)
     pr = synth.make_problem(cfg, seed=meta["seed_x"])
@@ -85,8 +85,9 @@ def _run(ctx, name, n, prec):
     h = bb.Hyper(cfg.kind, pr.log_ls, pr.log_s, pr.log_noise)
     ctx.set_matmul_precision(prec)
     try:
+        km = kmode if kmode is not None else (bb.STORED if cfg.stored else bb.ONTHEFLY)
         g = bb.mll_and_grad(ctx, X, y, h, cfg.t, cfg.k, cfg.p, seed=meta["seed_probes"],
-                            kmode=bb.STORED if cfg.stored else bb.ONTHEFLY, return_solves=True)
+                            kmode=km, return_solves=True)
     finally:
         ctx.set_matmul_precision(bb.INT8EXACT)
     U = g["U"].cpu().numpy()
@@ -135,6 +136,18 @@ def test_fullsize_grid31_c4(ctx, name, n):
     assert err["pivots_equal"] and g["stats"]["matmul_path"] == 2
     assert err["logdet"] <= 1e-3 and err["mll"] <= 1e-3, err
     assert err["solve"] <= 1e-4 and err["grad"] <= 1e-3, err
+
+
+@pytest.mark.parametrize("prec", [bb.INT8EXACT, bb.FP64ACC])
+def test_fullsize_c2_matern_on_the_fly(ctx, prec):
+    """C2 at its full size through the on-the-fly Matern-5/2 operator (K1-TC MODE 2, 39-bit D)
+    instead of the stored one, against the same cached oracle run: regime B, so the bars of
+    DESIGN.md §6a."""
+    meta, g, err = _run(ctx, "C2", 45730, prec, kmode=bb.ONTHEFLY)
+    assert err["pivots_equal"]
+    assert err["logdet"] <= 1e-3 and err["mll"] <= 1e-3, err
+    assert err["solve"] <= _regime_b_solve_bar("C2", 45730), err
+    assert err["grad"] <= REGIME_B_GRAD, err
 
 
 @pytest.mark.parametrize("name,n", CASES)
