@@ -85,8 +85,10 @@ typedef enum { BBMM_ONTHEFLY = 0, BBMM_STORED = 1 } bbmm_kmode_t;
  *   distance; any t + 1 <= 33 (padded to the next instantiated column block) with
  *   any d <= 32, and max |x_scaled|^2 <= 16 (precision guard).  On the fly,
  *   Matern-5/2: distances from direct fp32 differences (the expanded form's
- *   ~1e-7 error breaks the parity bars there), 23-bit kernel
- *   values, 39-bit D; t + 1 <= 17, d <= 14.  Stored K (BBMM_STORED, t + 1 <= 33):
+ *   ~1e-7 error breaks the parity bars there), kernel values on
+ *   the 31-bit grid and 55-bit D (23-bit / 39-bit under INT8EXACT23, which
+ *   misses the regime-B bars at full C2); t + 1 <= 64 (chunks of 17), d <= 14.
+ *   Stored K (BBMM_STORED, t + 1 <= 33):
  *   K built in fp64 and stored as 30-bit fixed point, D as 55-bit fixed point.
  *   Everything else uses FP64ACC.
  * INT8EXACT31 / INT8EXACT23: INT8EXACT with the on-the-fly RBF grid forced to
