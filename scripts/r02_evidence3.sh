@@ -10,6 +10,7 @@ timeout 1500 python bench.py > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.e
 timeout 1500 python bench.py --precision int8exact23 --no-cpu-baseline > gpurun_out/bench_C4_23.json 2> gpurun_out/bench_C4_23.err; tail -c 200 gpurun_out/bench_C4_23.json
 timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 200 gpurun_out/bench_ref.json
 for C in C1 C2 C3; do timeout 900 python bench.py --config $C --no-cpu-baseline > gpurun_out/bench_$C.json 2> gpurun_out/bench_$C.err; tail -c 150 gpurun_out/bench_$C.json; done
+timeout 900 python bench.py --config C2 --kmode onthefly --no-cpu-baseline > gpurun_out/bench_C2_otf.json 2> gpurun_out/bench_C2_otf.err; tail -c 150 gpurun_out/bench_C2_otf.json
 timeout 900 python scripts/bench_configs.py C0 C1 C2 C3 > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; cut -c1-150 gpurun_out/configs.jsonl
 timeout 900 python scripts/solve_residual_bound.py 131072 262144 1000000 > gpurun_out/resbound.jsonl 2> gpurun_out/resbound.err; cat gpurun_out/resbound.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C4.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1; tail -1 gpurun_out/launches_bench.log
