@@ -138,6 +138,17 @@ def test_fullsize_grid31_c4(ctx, name, n):
     assert err["solve"] <= 1e-4 and err["grad"] <= 1e-3, err
 
 
+def test_fullsize_23bit_grid_at_the_switch_point(ctx):
+    """The 23-bit k~ grid forced (INT8EXACT23) at the C4 shape, n = 262 144 -- just above the size
+    where the default switches to the 31-bit grid (sqrt(n) 5.3e-8 s / sigma^2 = 9.0e-5 > 0.8e-4):
+    the solve error there is the model's (residual estimate 8.7e-5), still inside the 1e-4 bar but
+    without the 20 % margin the switch keeps."""
+    meta, g, err = _run(ctx, "C4", 262144, bb.INT8EXACT23)
+    assert g["stats"]["kgrid_bits"] == 23 and err["pivots_equal"]
+    assert 0.6e-4 <= err["solve"] <= 1e-4, err
+    assert err["logdet"] <= 1e-3 and err["mll"] <= 1e-3 and err["grad"] <= 1e-3, err
+
+
 @pytest.mark.parametrize("prec", [bb.INT8EXACT, bb.FP64ACC])
 def test_fullsize_c2_matern_on_the_fly(ctx, prec):
     """C2 at its full size through the on-the-fly Matern-5/2 operator (K1-TC MODE 2, 39-bit D)
