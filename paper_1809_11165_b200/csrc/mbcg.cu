@@ -264,7 +264,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 }  // namespace
-constexpr int kL3T = 16, kL3Ld = 18, kL3St = 3;
+#ifndef BBMM_LTR3_T
+#define BBMM_LTR3_T 16
+#endif
+#ifndef BBMM_LTR3_ST
+#define BBMM_LTR3_ST 3
+#endif
+constexpr int kL3T = BBMM_LTR3_T, kL3Ld = BBMM_LTR3_T + 2, kL3St = BBMM_LTR3_ST;
 template <int MPT, int NT = 256>
 __global__ void __launch_bounds__(NT, 1)
 k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double *__restrict__ R,
@@ -290,7 +296,7 @@ k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
         const int rows = (int)min((int64_t)kL3T, i_end - i0);
         // L: k rows x 8 chunks of 2 doubles
         for (int e = threadIdx.x; e < k * (kL3T / 2); e += NT) {
-            const int m = e >> 3, q = e & 7;
+            const int m = e / (kL3T / 2), q = e % (kL3T / 2);
             const bool ok = 2 * q < rows;            // rows is even except at the very end
             const double *src = L + (int64_t)m * n + r0 + i0 + (ok ? 2 * q : 0);
             cp16(Ls + m * kL3Ld + 2 * q, src, ok ? (2 * q + 1 < rows ? 16 : 8) : 0);

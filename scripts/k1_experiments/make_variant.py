@@ -15,14 +15,15 @@ from paper_1809_11165_b200 import _build as B  # noqa: E402
 
 name, defs = sys.argv[1], sys.argv[2:]
 inc, libdir = B.nccl_paths()
-objs = [os.path.join(B.BUILD, f) for f in os.listdir(B.BUILD) if f.endswith(".o") and f != "k1tc2.cu.o"]
+SRC = os.environ.get("VARIANT_SRC", "k1tc2.cu")          # the source compiled with the -D flags
+objs = [os.path.join(B.BUILD, f) for f in os.listdir(B.BUILD) if f.endswith(".o") and f != SRC + ".o"]
 d = os.path.join(ROOT, "scratch", "var_" + name, "paper_1809_11165_b200")
 os.makedirs(os.path.join(d, "lib"), exist_ok=True)
 shutil.copy(os.path.join(ROOT, "paper_1809_11165_b200", "__init__.py"), d)
 o = os.path.join(ROOT, "scratch", "var_" + name, "k1tc2.o")
 subprocess.check_call([B.NVCC, "-std=c++17", "-O3", *B.ARCH, "-Xcompiler", "-fPIC", *defs, "-I", inc,
                        "-I", B.CSRC, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
-                       "-c", os.path.join(B.CSRC, "k1tc2.cu"), "-o", o])
+                       "-c", os.path.join(B.CSRC, SRC), "-o", o])
 subprocess.check_call([B.NVCC, "-shared", *B.ARCH, "-o", os.path.join(d, "lib", "libbbmm.so"), o, *objs,
                        "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}"])
 os.remove(o)
