@@ -55,6 +55,26 @@ struct Error {
 
 #define BBMM_LAUNCH_CHECK() BBMM_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the newer kernels (a build with -DBBMM_BOUNDS_CHECK traps on a
+// violated index; compute-sanitizer is not available on the GPU pool): off in the product build.
+#ifdef BBMM_BOUNDS_CHECK
+#define BBMM_DCHECK(cond)                                                                   \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("BBMM_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,  \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                            \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define BBMM_DCHECK(cond) ((void)0)
+#endif
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+
 // ------------------------------------------------------- kernel parameters
 // Input-space scaling so the pair kernels evaluate k from a scaled distance:
 //   RBF:    xs = x * sqrt(log2(e)/2) / l   ->  k = s * 2^(-|xs_i - xs_j|^2)

@@ -304,6 +304,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    BBMM_DCHECK((uint32_t)K::SMEM <= dyn_smem_bytes() && K::END <= 512);
 
     if (warp == PRODUCER_WARP) {
         // ------------------------------------------------------- producer
@@ -743,6 +744,7 @@ k1tc2_rbf(const float *__restrict__ Xa, const float *__restrict__ XB,
             constexpr int CS = (C + 3) & ~3;
             const int rl = sub * 32 + lane;
             double *out = Vpart + ((int64_t)blockIdx.y * nloc + row) * ldv + coff;
+            BBMM_DCHECK(coff + C <= ldv);
             const double base = s * (ND == 4 ? 0x1p-53 : ND == 5 ? 0x1p-61 : 0x1p-77) *
                                 (MODE == 1 ? 1.3862943611198906 : 1.0);   // MODE 1: r^2 = -2 ln2 S
             const double cacc = acc_sm[C][rl];

@@ -278,6 +278,7 @@ k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
     extern __shared__ __align__(16) double sm_l3[];
     const int stage_d = k * kL3Ld + kL3T * c + 2;      // doubles per stage (keep 16-B alignment)
     const int stage = (stage_d + 1) & ~1;
+    BBMM_DCHECK((size_t)kL3St * stage * 8 <= dyn_smem_bytes());
     const int CGN = (c + 3) / 4, MLN = NT / CGN;
     const int g = threadIdx.x % CGN, ml = threadIdx.x / CGN;
     const bool act = ml < MLN;
@@ -299,6 +300,7 @@ k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
             const int m = e / (kL3T / 2), q = e % (kL3T / 2);
             const bool ok = 2 * q < rows;            // rows is even except at the very end
             const double *src = L + (int64_t)m * n + r0 + i0 + (ok ? 2 * q : 0);
+            BBMM_DCHECK(m < k && r0 + i0 + (ok ? 2 * q + (2 * q + 1 < rows ? 2 : 1) : 0) <= n);
             cp16(Ls + m * kL3Ld + 2 * q, src, ok ? (2 * q + 1 < rows ? 16 : 8) : 0);
         }
         // R: rows x c doubles, contiguous
@@ -306,6 +308,7 @@ k_LtR3(const double *__restrict__ L, int64_t n, int64_t r0, int k, const double 
         for (int e = threadIdx.x; e < rchunks; e += NT) {
             const int o = 2 * e;
             const int nb = o + 1 < rd ? 16 : (o < rd ? 8 : 0);
+            BBMM_DCHECK(i0 * c + (nb ? o + nb / 8 : 0) <= nloc * c);
             cp16(Rs + o, R + i0 * c + (nb ? o : 0), nb);
         }
     };
@@ -428,6 +431,7 @@ k_sor_expand2(const double *__restrict__ Bs, int64_t n, int64_t r0, int m,
               const double *__restrict__ T, int64_t nloc, int c, int cs, double *__restrict__ Vpart) {
     constexpr int CP = (CMAX + 1) & ~1;
     extern __shared__ __align__(16) double Tp[];   // m x CP (zero padded)
+    BBMM_DCHECK((uint32_t)m * CP * 8 <= dyn_smem_bytes());
     for (int e = threadIdx.x; e < m * CP; e += blockDim.x) {
         const int a = e / CP, u = e - a * CP;
         Tp[e] = u < c ? T[a * c + u] : 0.0;
