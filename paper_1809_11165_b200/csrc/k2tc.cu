@@ -105,6 +105,30 @@ struct InvLs {
     double v[kMaxDim];   // 1 / l_q (ARD) or 1 / l repeated, 0 past d
 };
 
+// exp(x) for x <= 0 in fp64 without libdevice's special-case paths: x = k ln2 + r (Cody-Waite,
+// |r| <= ln2 / 2), exp(r) by its Taylor polynomial of degree 10 (truncation < 3e-13 relative),
+// times 2^k through the exponent field; 0 below -708 (far under the 2^-30 grid of the stored K).
+// The stored kernel values are rounded to 30-bit fixed point, so this keeps them exact to the
+// grid while costing ~13 fp64 FMA-pipe ops instead of the general exp's range checks.
+__device__ __forceinline__ double exp_nonpos(double x) {
+    if (x < -708.0) return 0.0;
+    const double kd = rint(x * 1.4426950408889634);
+    double r = fma(kd, -6.93147180369123816490e-01, x);
+    r = fma(kd, -1.90821492927058770002e-10, r);
+    double p = 2.7557319223985893e-07;                 // 1/10!
+    p = fma(p, r, 2.7557319223985888e-06);             // 1/9!
+    p = fma(p, r, 2.4801587301587302e-05);             // 1/8!
+    p = fma(p, r, 1.9841269841269841e-04);             // 1/7!
+    p = fma(p, r, 1.3888888888888889e-03);             // 1/6!
+    p = fma(p, r, 8.3333333333333332e-03);             // 1/5!
+    p = fma(p, r, 4.1666666666666664e-02);             // 1/4!
+    p = fma(p, r, 1.6666666666666666e-01);             // 1/3!
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    return p * __longlong_as_double((long long)((int)kd + 1023) << 52);
+}
+
 template <int KIND, int D>
 __global__ void __launch_bounds__(BM)
 k_build_kq64(const float *__restrict__ X, int d, InvLs il, int64_t n, int64_t r0, int64_t nloc,
@@ -145,10 +169,10 @@ k_build_kq64(const float *__restrict__ X, int d, InvLs il, int64_t n, int64_t r0
                     if (r0 + i == j) {
                         kv = 1.0;                        // K_ii = s exactly
                     } else if (KIND == 0) {
-                        kv = exp(-0.5 * r2);
+                        kv = exp_nonpos(-0.5 * r2);
                     } else {
                         const double sr = sqrt(5.0 * r2);
-                        kv = (1.0 + sr + (5.0 / 3.0) * r2) * exp(-sr);
+                        kv = (1.0 + sr + (5.0 / 3.0) * r2) * exp_nonpos(-sr);
                     }
                 }
                 q[v] = __double2uint_rn(kv * 1073741824.0);
