@@ -592,3 +592,25 @@ def test_column_chunks_kernel_matmul(ctx, orc, name, c):
     err = np.abs(V - ref)
     bound = matmul_bound(orc, pr, D)
     assert np.all(err <= bound), float((err / bound).max())
+
+
+@pytest.mark.parametrize("n,c", [(2777, 17), (1500, 11)])
+def test_matern_23bit_grid_mode2_matches_oracle(ctx, orc, n, c):
+    """Matern-5/2 on the fly with the 23-bit grid forced (INT8EXACT23: K1-TC MODE 2, 39-bit D) --
+    the default is MODE 4 (31-bit grid, 55-bit D); MODE 2 stays available and is held to the
+    element-wise matmul bound and the MLL bars at these (regime-A-like) sizes."""
+    pr = synth.make_problem(synth.scaled(synth.CONFIGS["C2"], n), seed=3)
+    D = synth.random_block(n, c, seed=4).astype(np.float64)
+    ctx.set_matmul_precision(bb.INT8EXACT23)
+    try:
+        V = bb.kernel_matmul(ctx, dev(pr.X), dev(D, torch.float64), hyper_of(pr), bb.ONTHEFLY).cpu().numpy()
+    finally:
+        ctx.set_matmul_precision(bb.INT8EXACT)
+    ref = orc.kernel_matmul(pr.cfg.kind, pr.X, pr.log_ls, pr.log_s, pr.log_noise, D)
+    bound = matmul_bound(orc, pr, D)
+    assert np.all(np.abs(V - ref) <= bound)
+    cfg = synth.dataclasses.replace(synth.CONFIGS["C2"], n=1200, t=c - 1)
+    _, g, o = run_both(ctx, orc, cfg, kmode=bb.ONTHEFLY, prec=bb.INT8EXACT23)
+    assert g["stats"]["matmul_path"] == 2 and g["stats"]["kgrid_bits"] == 23
+    assert abs(g["mll"] - o["mll"]) <= 1e-3 * abs(o["mll"])
+    assert np.linalg.norm(g["grad"] - o["grad"]) <= 1e-3 * np.linalg.norm(o["grad"])
