@@ -25,7 +25,7 @@ import oracle  # noqa: E402
 import paper_1809_11165_b200 as bb  # noqa: E402
 import synth  # noqa: E402
 
-M_ROWS = 512
+M_ROWS = int(os.environ.get("RESBOUND_ROWS", "512"))
 
 
 def run(ctx, n, prec, label):
